@@ -1,0 +1,219 @@
+/*
+ * qrmark_gpu.h — C-ABI of the B200-native QRMark tile-detection path.
+ *
+ * This is the drop-in boundary: plain C types, plain pointers and sizes, no
+ * C++ or torch types. Each entry point names the reference interface it
+ * replaces (paths relative to /root/reference/proj). The C++ drop-in API
+ * (include/qrmark/*.hpp, namespace qrmark) and the Python package
+ * (paper_2509_02447_b200) are both thin layers over these calls.
+ *
+ * Conventions
+ *  - Status codes only; no exception crosses the ABI. The C++ layer maps
+ *    QRM_INVALID_INPUT / QRM_DIVISION_BY_ZERO / QRM_INFEASIBLE back to the
+ *    reference exceptions (include/qrmark/errors.hpp:11-25). qrm_last_error()
+ *    returns the message of the calling thread's last failure.
+ *  - Packed words: a codeword / message of <= 64 bits is a uint64_t holding bit
+ *    0 of the reference BitVec (rs.hpp:16) in its most significant used bit,
+ *    i.e. word = sum_b bit[b] << (nbits-1-b). Symbols are MSB-first m-bit
+ *    groups (rs.cpp:8-25).
+ *  - "_device" calls take device pointers and a cudaStream_t passed as void*
+ *    (NULL = legacy default stream); they are stream-ordered and asynchronous.
+ *    "_host" calls take host pointers and return when results are in host
+ *    memory.
+ *  - One context per device and host thread; a context is not thread-safe.
+ *  - There is no CPU fallback: every compute call runs on the GPU and fails
+ *    with QRM_CUDA_ERROR / QRM_NO_DEVICE when it cannot.
+ */
+#ifndef QRMARK_GPU_H
+#define QRMARK_GPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#define QRM_EXPORT __attribute__((visibility("default")))
+#else
+#define QRM_EXPORT
+#endif
+
+typedef enum qrm_status {
+    QRM_OK = 0,
+    QRM_INVALID_INPUT = 1,    /* qrmark::InvalidInput    (errors.hpp:11) */
+    QRM_DIVISION_BY_ZERO = 2, /* qrmark::DivisionByZero  (errors.hpp:16) */
+    QRM_INFEASIBLE = 3,       /* qrmark::InfeasibleConfig (errors.hpp:22) */
+    QRM_CUDA_ERROR = 4,
+    QRM_NO_DEVICE = 5,
+    QRM_INTERNAL = 6
+} qrm_status;
+
+/* TileStrategy (tiling.hpp:13) */
+enum { QRM_TILE_RANDOM = 0, QRM_TILE_RANDOM_GRID = 1, QRM_TILE_FIXED = 2 };
+
+/* Record status */
+enum { QRM_REC_FAILED = 0, QRM_REC_DECODED = 1 };
+
+/* DetectionConfig (detect.hpp:25-37) + CodeParams (rs.hpp:26-37). */
+typedef struct qrm_config {
+    int symbol_bits;            /* m: 4 (GF(16), poly 0x13) or 8 (GF(256), poly 0x11D) */
+    int n, k;                   /* code length / dimension, X_i = alpha^i (rs.cpp:52-63) */
+    int tile_size;              /* l (TileSpec::size, tiling.hpp:16-20) */
+    int tile_strategy;          /* QRM_TILE_* */
+    uint64_t tile_seed;         /* TileSpec::seed */
+    uint64_t key_seed;          /* WatermarkKey::seed (stego.hpp:15-19) */
+    double alpha;               /* WatermarkKey::alpha */
+    const uint8_t* key_message; /* k*m bits, one 0/1 byte per bit (host memory) */
+    double fpr_target;          /* DetectionConfig::fpr_target */
+} qrm_config;
+
+/* DetectionRecord (detect.hpp:45-55), compact device form. bit_acc =
+ * matches / (n*m); corrected present iff status == QRM_REC_DECODED. */
+typedef struct qrm_record {
+    uint64_t raw;      /* hardened extractor output m' (packed) */
+    uint64_t msg;      /* RS-corrected information bits c_s (packed), 0 on failure */
+    uint8_t status;    /* QRM_REC_* */
+    uint8_t errors;    /* errors_corrected (0 on failure) */
+    uint8_t matches;   /* raw vs key codeword matching bits */
+    uint8_t verified;  /* detect.cpp:186-195 */
+    uint8_t ties;      /* correlations that were exactly zero (resolved bit-exactly) */
+    uint8_t reserved[3];
+} qrm_record;
+
+/* StreamPlan (sched.hpp:26-34) for the 3-stage host pipeline. */
+typedef struct qrm_plan {
+    int streams[3];   /* s[k]: transfer / decode / correct+return */
+    int minibatch[3]; /* m[k] */
+} qrm_plan;
+
+/* Per-call stage timings of qrm_detect_host (cudaEvent based, ms). */
+typedef struct qrm_host_stats {
+    double wall_ms;
+    double h2d_bytes;
+    double d2h_bytes;
+    int minibatches;
+    int kernel_launches;
+} qrm_host_stats;
+
+typedef struct qrm_ctx qrm_ctx;
+
+QRM_EXPORT const char* qrm_last_error(void);
+QRM_EXPORT int qrm_abi_version(void);
+QRM_EXPORT int qrm_device_count(void);
+
+/* ---------------------------------------------------------------- context
+ * Replaces DetectionContext::DetectionContext (detect.cpp:135-146) and the
+ * SpreadSpectrumCodec constructor (stego.cpp:16-27): validates the config,
+ * builds the +-1 pattern planes on the device, the GF tables, the key
+ * codeword (rs_encode, rs.cpp:78-91) and the verify thresholds
+ * (verify_threshold, detect.cpp:31-66). */
+QRM_EXPORT qrm_status qrm_ctx_create(int device, const qrm_config* cfg, qrm_ctx** out);
+QRM_EXPORT void qrm_ctx_destroy(qrm_ctx* ctx);
+/* Key codeword (packed) and thresholds tau(k*m), tau(n*m) of the context. */
+QRM_EXPORT qrm_status qrm_ctx_info(const qrm_ctx* ctx, uint64_t* key_codeword, uint64_t* key_message, int* tau_msg,
+                                   int* tau_raw);
+
+/* ----------------------------------------------------------------- detect
+ * Replaces detect_batch (detect.cpp:250-368) / DetectionContext::detect_one
+ * (detect.cpp:164-198) for a uniform batch: `count` images of w x h RGB u8,
+ * interleaved HWC (image.hpp:28-30), image i at images + i*image_stride.
+ * draw_index of image i = first_draw + i (tiling.cpp:40). Device-resident:
+ * `images` and `out` are device pointers (or mapped pinned host memory). */
+QRM_EXPORT qrm_status qrm_detect_device(qrm_ctx* ctx, const uint8_t* images, int64_t count, int w, int h,
+                                        int64_t image_stride, uint64_t first_draw, qrm_record* out, void* stream);
+
+/* Same, from HOST images to HOST records, through the stream pipeline (the
+ * CUDA-stream executor that replaces detect_batch's thread pools and bounded
+ * queues). plan == NULL uses the context's current plan (qrm_ctx_set_plan).
+ * mode 0: window-only transfer (the tile window is read from mapped pinned host
+ * memory by the decode kernel); mode 1: full-image H2D copies. Host images are
+ * registered (page-locked) for the call if they are not pinned already. */
+QRM_EXPORT qrm_status qrm_detect_host(qrm_ctx* ctx, const uint8_t* images, int64_t count, int w, int h,
+                                      int64_t image_stride, uint64_t first_draw, qrm_record* out,
+                                      const qrm_plan* plan, int mode, qrm_host_stats* stats);
+
+/* Ragged batch (std::span<const ImageBuffer> of mixed sizes, detect.hpp:145):
+ * per-image host pointers and sizes. Images smaller than 256 px take the
+ * bilinear upscale path (transforms.cpp:24-47). */
+QRM_EXPORT qrm_status qrm_detect_ragged(qrm_ctx* ctx, const uint8_t* const* images, const int* widths,
+                                        const int* heights, int64_t count, uint64_t first_draw, qrm_record* out);
+
+/* SpreadSpectrumCodec::extract + harden (stego.cpp:10-14, 53-67) for a
+ * uniform device batch: soft (count x n*m doubles, nullable) and raw words.
+ * soft_i = S_i / (255 * 3 l^2) with S_i the exact integer correlation. */
+QRM_EXPORT qrm_status qrm_extract_device(qrm_ctx* ctx, const uint8_t* images, int64_t count, int w, int h,
+                                         int64_t image_stride, uint64_t first_draw, double* soft, uint64_t* raw,
+                                         void* stream);
+
+/* preprocess (transforms.cpp:42-47) of one host image -> 256*256*3 floats. */
+QRM_EXPORT qrm_status qrm_preprocess_host(const uint8_t* image, int w, int h, float* out);
+
+/* ----------------------------------------------------------------- RS
+ * Replace bw_decode (rs.cpp:188-196), bit-exact: the unique codeword within
+ * distance t or failure. nerr_out[i] = errors_corrected, or -1 for a decode
+ * failure (nullopt). */
+/* Packed words (n*m <= 64). algo 0: auto; 1: thread-per-codeword syndrome
+ * decoder (t = 1 codes); 2: warp-per-codeword Berlekamp-Massey/Chien/Forney. */
+QRM_EXPORT qrm_status qrm_rs_decode_packed_device(int m, int n, int k, const uint64_t* words, int64_t count,
+                                                  uint64_t* cw_out, int8_t* nerr_out, int algo, void* stream);
+/* Symbol arrays (any n <= 2^m - 1, m in {4, 8}): count*n bytes in/out. */
+QRM_EXPORT qrm_status qrm_rs_decode_symbols_device(int m, int n, int k, const uint8_t* recv, int64_t count,
+                                                   uint8_t* cw_out, int8_t* nerr_out, void* stream);
+/* RS stress words (SURVEY 8d recipe) on the device: per word a random message,
+ * its codeword with e injected symbol errors (e <= t for 90%, t+1..3 for 10%). */
+QRM_EXPORT qrm_status qrm_rs_stress_device(int m, int n, int k, uint64_t seed, int64_t count, uint64_t* msg,
+                                           uint64_t* words, int8_t* nerr_true, void* stream);
+/* rs_encode (rs.cpp:78-91) on the host, packed (n*m <= 64). */
+QRM_EXPORT qrm_status qrm_rs_encode_packed(int m, int n, int k, uint64_t message, uint64_t* codeword);
+/* verify_threshold (detect.cpp:31-66). */
+QRM_EXPORT qrm_status qrm_verify_threshold(int n_bits, double fpr, int* tau);
+
+/* ----------------------------------------------------------------- inputs
+ * Synthetic corpus on the device (cmd_bench recipe, cli.cpp:404-411):
+ * image i = synthetic_image(first_seed + i, w, h) (image.cpp:157-189),
+ * optionally normalize -> embed_image_grid (stego.cpp:77-92) with the key
+ * codeword -> denormalize. Output u8 [count][h][w][3] at `out` (device). */
+QRM_EXPORT qrm_status qrm_make_corpus_device(const qrm_config* cfg, uint64_t first_seed, int64_t count, int w,
+                                             int h, int embed, uint8_t* out, void* stream);
+/* The codec's +-1 planes (stego.cpp:22-26), n_bits x 3l^2 int8 (device). */
+QRM_EXPORT qrm_status qrm_patterns_device(uint64_t key_seed, int n_bits, int l, int8_t* out, void* stream);
+
+/* ------------------------------------------------------------- scheduler
+ * allocate_streams (sched.cpp:50-114): Algorithm 1. */
+QRM_EXPORT qrm_status qrm_allocate_streams(int stages, const double* time, const double* memory, double b0,
+                                           int global_batch, int stream_budget, double m_cap, double epsilon,
+                                           int stall_cap, int* streams_out, int* minibatch_out,
+                                           double* bottleneck_out);
+/* lpt_schedule (sched.cpp:177-235): Algorithm 2. Pieces are returned stream
+ * by stream in placement order. */
+QRM_EXPORT qrm_status qrm_lpt_schedule(int ntasks, const int* ids, const double* latency, const double* memory,
+                                       const int* units, int stream_count, double lambda, double m_cap, int b_min,
+                                       int global_batch, int capacity, int* p_stream, int* p_id, int* p_units,
+                                       double* p_latency, double* p_memory, int* p_mb, int* n_pieces,
+                                       double* loads, int* m_unit);
+/* warmup_profile (sim.cpp:240-288): cudaEvent-timed warm-up of the three
+ * device stages (transfer, decode, correct) at baseline batch b0 on `images`
+ * (host, uniform w x h). Fills time[3] (ms per b0 images), memory[3] (bytes
+ * per image). */
+QRM_EXPORT qrm_status qrm_warmup_profile(qrm_ctx* ctx, const uint8_t* images, int64_t count, int w, int h,
+                                         int64_t image_stride, int warmup_iters, int b0, double* time,
+                                         double* memory);
+/* Sets the plan used by qrm_detect_host when its plan argument is NULL. */
+QRM_EXPORT qrm_status qrm_ctx_set_plan(qrm_ctx* ctx, const qrm_plan* plan);
+
+/* Measurement hook: runs the device detect path `reps` times on a uniform
+ * device batch and returns the mean duration of the decode kernel alone
+ * (cudaEvents recorded on its stream immediately around each launch). */
+QRM_EXPORT qrm_status qrm_probe_decode_kernel(qrm_ctx* ctx, const uint8_t* images, int64_t count, int w, int h,
+                                              int64_t image_stride, int reps, double* avg_ms);
+
+/* Number of kernels this library has launched in the calling process. */
+QRM_EXPORT uint64_t qrm_kernel_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* QRMARK_GPU_H */

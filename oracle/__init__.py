@@ -107,9 +107,13 @@ class DetectCfg:
     alpha: float = 0.04
     fpr: float = 1e-6
     key_message: np.ndarray | None = None  # defaults to default_message(key_seed)
+    mnk: tuple | None = None  # explicit (m, n, k), overriding the profile (CodeParams::make)
 
     @property
     def code(self):
+        if self.mnk is not None:
+            m, n, k = self.mnk
+            return m, n, k, (n - k) // 2
         return profile_params(self.profile, self.payload_bits)
 
 

@@ -1,0 +1,844 @@
+// C-ABI implementation (include/qrmark_gpu.h): context, device-resident and
+// host-buffer detection, RS batch decode, corpus generation, planners.
+//
+// The host-buffer path (qrm_detect_host) is the CUDA-stream executor that
+// replaces detect_batch's three thread pools and bounded queues
+// (detect.cpp:250-368): the batch is cut into mini-batches that flow through
+// three stages — transfer (H2D copy engine, or nothing when the decode kernel
+// reads the tile window straight out of mapped pinned host memory), decode
+// (tcgen05 correlation + fused harden/RS/verify) and correct/return (tie /
+// general-t completion kernel + D2H of the compact records) — with stage k
+// round-robining its mini-batches over plan.streams[k] CUDA streams and
+// cudaEvents instead of queues between stages.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "host_code.hpp"
+#include "qrm_device.cuh"
+#include "qrm_types.h"
+#include "qrmark_gpu.h"
+#include "sched_host.hpp"
+
+namespace qrm {
+cudaError_t launch_corr_detect(const DetectParams& p, cudaStream_t st);
+cudaError_t launch_detect_finish(const DetectParams& p, int tmax, int sm_count, cudaStream_t st);
+cudaError_t launch_gather_windows(const GatherDesc* descs, int64_t count, int l, uint8_t* out, cudaStream_t st);
+cudaError_t launch_rs_packed(const RsTables* tab, int t, int algo, const uint64_t* words, int64_t count, uint64_t* cw,
+                             int8_t* nerr, int sm_count, cudaStream_t st);
+cudaError_t launch_rs_symbols(const RsTables* tab, int n, int t, const uint8_t* recv, int64_t count, uint8_t* cw,
+                              int8_t* nerr, int sm_count, cudaStream_t st);
+cudaError_t launch_rs_stress(const RsTables* tab, const uint64_t* enc_mask, uint64_t seed, int64_t count,
+                             uint64_t* msg, uint64_t* words, int8_t* nerr_true, cudaStream_t st);
+cudaError_t launch_build_patterns(uint64_t seed, int nbits, int K, int K_pad, int8_t* pat, int32_t* colsum,
+                                  cudaStream_t st);
+cudaError_t launch_residual(uint64_t seed, int nbits, int K, uint64_t codeword, float* delta, cudaStream_t st);
+cudaError_t launch_corpus(uint64_t first_seed, int64_t count, int w, int h, int l, int embed, float alpha,
+                          const float* delta, uint8_t* out, cudaStream_t st);
+}  // namespace qrm
+
+using namespace qrm;
+
+namespace {
+
+thread_local std::string g_err;
+std::atomic<uint64_t> g_launches{0};
+
+qrm_status fail(qrm_status s, const std::string& msg) {
+    g_err = msg;
+    return s;
+}
+
+#define QRM_CUDA(call)                                                                          \
+    do {                                                                                        \
+        cudaError_t e_ = (call);                                                                \
+        if (e_ != cudaSuccess)                                                                  \
+            return fail(QRM_CUDA_ERROR, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+    } while (0)
+
+#define QRM_LAUNCH(call)       \
+    do {                       \
+        QRM_CUDA(call);        \
+        g_launches.fetch_add(1); \
+    } while (0)
+
+cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+int64_t now_ns() {
+    return std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now().time_since_epoch())
+        .count();
+}
+
+// Device RS tables per (device, m, n, k), built once.
+std::mutex g_tab_mu;
+std::map<std::tuple<int, int, int, int>, RsTables*> g_tabs;
+
+qrm_status rs_tables_for(int m, int n, int k, const RsTables** out) {
+    int dev = 0;
+    QRM_CUDA(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lock(g_tab_mu);
+    auto key = std::make_tuple(dev, m, n, k);
+    auto it = g_tabs.find(key);
+    if (it != g_tabs.end()) {
+        *out = it->second;
+        return QRM_OK;
+    }
+    RsTables h;
+    build_rs_tables(m, n, k, h);
+    RsTables* d = nullptr;
+    QRM_CUDA(cudaMalloc(&d, sizeof(RsTables)));
+    QRM_CUDA(cudaMemcpy(d, &h, sizeof(RsTables), cudaMemcpyHostToDevice));
+    g_tabs[key] = d;
+    *out = d;
+    return QRM_OK;
+}
+
+template <typename T>
+qrm_status ensure(T*& ptr, int64_t& cap, int64_t need) {
+    if (need <= cap) return QRM_OK;
+    if (ptr) cudaFree(ptr);
+    ptr = nullptr;
+    cap = 0;
+    const int64_t n = std::max<int64_t>(need, 1);
+    QRM_CUDA(cudaMalloc(&ptr, sizeof(T) * n));
+    cap = n;
+    return QRM_OK;
+}
+
+struct Workspace {
+    int32_t* pending_count = nullptr;
+    PendingEntry* pending = nullptr;
+    int64_t pending_cap = 0;
+    uint8_t* stage = nullptr;  // gathered windows (staged path)
+    int64_t stage_cap = 0;
+    GatherDesc* descs = nullptr;
+    int64_t desc_cap = 0;
+    uint8_t* images = nullptr;  // full-image H2D buffer (host pipeline, mode 1)
+    int64_t images_cap = 0;
+    void release() {
+        cudaFree(pending_count);
+        cudaFree(pending);
+        cudaFree(stage);
+        cudaFree(descs);
+        cudaFree(images);
+        *this = Workspace{};
+    }
+};
+
+}  // namespace
+
+struct qrm_ctx {
+    int device = 0;
+    int sms = 148;
+    qrm_config cfg{};
+    std::vector<uint8_t> key_message;
+    int m = 0, n = 0, k = 0, t = 0, nbits = 0, kbits = 0, l = 0, K = 0, K_pad = 0;
+    uint64_t key_cw = 0, key_msg = 0;
+    int tau_msg = 0, tau_raw = 0;
+    int8_t* d_patterns = nullptr;
+    int32_t* d_colsum = nullptr;
+    const RsTables* d_rs = nullptr;
+    qrm_record* d_records = nullptr;
+    int64_t records_cap = 0;
+    std::vector<Workspace> ws;  // [0]: device API; [1..]: host pipeline slots
+    std::vector<cudaStream_t> streams;
+    qrm_plan plan{{1, 2, 1}, {4096, 4096, 4096}};
+};
+
+namespace {
+
+qrm_status workspace_reserve(Workspace& w, int64_t count) {
+    qrm_status s;
+    if (!w.pending_count) QRM_CUDA(cudaMalloc(&w.pending_count, sizeof(int32_t)));
+    if ((s = ensure(w.pending, w.pending_cap, count)) != QRM_OK) return s;
+    return QRM_OK;
+}
+
+// Geometry of preprocess (transforms.cpp:24-38).
+void geometry(int w, int h, int& up, int& sw, int& sh, int& xo, int& yo) {
+    const int mn = std::min(w, h);
+    if (mn < kWorkingSize) {
+        const double s = static_cast<double>(kWorkingSize) / mn;
+        up = 1;
+        sw = std::max<int>(kWorkingSize, static_cast<int>(std::lround(w * s)));
+        sh = std::max<int>(kWorkingSize, static_cast<int>(std::lround(h * s)));
+    } else {
+        up = 0;
+        sw = w;
+        sh = h;
+    }
+    xo = (sw - kWorkingSize) / 2;
+    yo = (sh - kWorkingSize) / 2;
+}
+
+DetectParams base_params(qrm_ctx* c, Workspace& w, int64_t count, qrm_record* out, double* soft, uint64_t* raw) {
+    DetectParams p{};
+    p.count = count;
+    p.K = c->K;
+    p.K_pad = c->K_pad;
+    p.nbits = c->nbits;
+    p.kbits = c->kbits;
+    p.tau_msg = c->tau_msg;
+    p.tau_raw = c->tau_raw;
+    p.fuse_t1 = (c->t == 1 && c->n - c->k <= 3) ? 1 : 0;
+    p.key_cw = c->key_cw;
+    p.key_msg = c->key_msg;
+    p.patterns = c->d_patterns;
+    p.colsum = c->d_colsum;
+    p.rs = c->d_rs;
+    p.out = out;
+    p.soft = soft;
+    p.raw_out = raw;
+    p.pending_count = w.pending_count;
+    p.pending = w.pending;
+    return p;
+}
+
+// Decode + correct `count` windows described by src into device records.
+cudaEvent_t g_probe[2] = {nullptr, nullptr};  // set only by qrm_probe_decode_kernel
+
+qrm_status run_detect(qrm_ctx* c, Workspace& w, const WindowSource& src, int64_t count, qrm_record* out,
+                      double* soft, uint64_t* raw, cudaStream_t st, cudaEvent_t mid_event = nullptr,
+                      cudaStream_t finish_stream = nullptr) {
+    qrm_status s = workspace_reserve(w, count);
+    if (s != QRM_OK) return s;
+    DetectParams p = base_params(c, w, count, out, soft, raw);
+    p.src = src;
+    QRM_CUDA(cudaMemsetAsync(w.pending_count, 0, sizeof(int32_t), st));
+    if (g_probe[0]) QRM_CUDA(cudaEventRecord(g_probe[0], st));
+    QRM_LAUNCH(launch_corr_detect(p, st));
+    if (g_probe[1]) QRM_CUDA(cudaEventRecord(g_probe[1], st));
+    cudaStream_t fs = st;
+    if (mid_event && finish_stream) {
+        QRM_CUDA(cudaEventRecord(mid_event, st));
+        QRM_CUDA(cudaStreamWaitEvent(finish_stream, mid_event, 0));
+        fs = finish_stream;
+    }
+    QRM_LAUNCH(launch_detect_finish(p, std::max(1, c->t), c->sms, fs));
+    return QRM_OK;
+}
+
+bool direct_ok(const qrm_ctx* c, const uint8_t* base, int w, int h, int64_t stride) {
+    int up, sw, sh, xo, yo;
+    geometry(w, h, up, sw, sh, xo, yo);
+    if (up) return false;
+    if (c->cfg.tile_strategy == QRM_TILE_RANDOM) return false;
+    const int pitch = w * 3;
+    if (reinterpret_cast<uintptr_t>(base) % 16 || stride % 16 || pitch % 16) return false;
+    if ((xo * 3) % 16 || (c->l * 3) % 16) return false;
+    return true;
+}
+
+// Uniform batch at `images` (device-accessible) -> records, choosing the direct
+// window path when alignment allows and the gather path otherwise.
+qrm_status detect_uniform(qrm_ctx* c, Workspace& w, const uint8_t* images, int64_t count, int width, int height,
+                          int64_t stride, uint64_t first_draw, qrm_record* out, double* soft, uint64_t* raw,
+                          cudaStream_t st, cudaEvent_t mid = nullptr, cudaStream_t fs = nullptr) {
+    if (count == 0) return QRM_OK;
+    int up, sw, sh, xo, yo;
+    geometry(width, height, up, sw, sh, xo, yo);
+    WindowSource src{};
+    src.l = c->l;
+    src.strategy = c->cfg.tile_strategy;
+    src.tile_seed = c->cfg.tile_seed;
+    src.first_draw = first_draw;
+    if (direct_ok(c, images, width, height, stride)) {
+        src.base = images;
+        src.image_stride = stride;
+        src.pitch = width * 3;
+        src.x_off = xo;
+        src.y_off = yo;
+        src.direct = 1;
+    } else {
+        qrm_status s;
+        if ((s = ensure(w.stage, w.stage_cap, count * c->K)) != QRM_OK) return s;
+        if ((s = ensure(w.descs, w.desc_cap, count)) != QRM_OK) return s;
+        std::vector<GatherDesc> d(count);
+        for (int64_t i = 0; i < count; ++i) {
+            int tx, ty;
+            select_tile(kWorkingSize, kWorkingSize, c->l, c->cfg.tile_strategy, c->cfg.tile_seed,
+                        first_draw + static_cast<uint64_t>(i), tx, ty);
+            d[i] = GatherDesc{images + i * stride, width, height, up, sw, sh, xo, yo, tx, ty};
+        }
+        QRM_CUDA(cudaMemcpyAsync(w.descs, d.data(), sizeof(GatherDesc) * count, cudaMemcpyHostToDevice, st));
+        QRM_LAUNCH(launch_gather_windows(w.descs, count, c->l, w.stage, st));
+        QRM_CUDA(cudaStreamSynchronize(st));  // the pageable descriptor copy must finish before `d` dies
+        src.base = w.stage;
+        src.image_stride = c->K;
+        src.pitch = 3 * c->l;
+        src.direct = 0;
+    }
+    return run_detect(c, w, src, count, out, soft, raw, st, mid, fs);
+}
+
+qrm_status check_uniform(const qrm_ctx* c, const uint8_t* images, int64_t count, int w, int h, int64_t stride) {
+    if (!c) return fail(QRM_INVALID_INPUT, "null context");
+    if (count < 0) return fail(QRM_INVALID_INPUT, "negative image count");
+    if (count > 0 && !images) return fail(QRM_INVALID_INPUT, "null image pointer");
+    if (w <= 0 || h <= 0) return fail(QRM_INVALID_INPUT, "image dimensions must be positive");
+    if (stride < static_cast<int64_t>(w) * h * 3) return fail(QRM_INVALID_INPUT, "image stride smaller than an image");
+    return QRM_OK;
+}
+
+qrm_status set_device(int dev) {
+    QRM_CUDA(cudaSetDevice(dev));
+    return QRM_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+QRM_EXPORT const char* qrm_last_error(void) { return g_err.c_str(); }
+QRM_EXPORT int qrm_abi_version(void) { return 1; }
+QRM_EXPORT uint64_t qrm_kernel_launch_count(void) { return g_launches.load(); }
+
+QRM_EXPORT int qrm_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) return 0;
+    return n;
+}
+
+QRM_EXPORT qrm_status qrm_verify_threshold(int n_bits, double fpr, int* tau) {
+    const int v = verify_threshold(n_bits, fpr);
+    if (v < 0) return fail(QRM_INVALID_INPUT, "verify threshold needs n_bits > 0 and fpr in (0, 1)");
+    *tau = v;
+    return QRM_OK;
+}
+
+QRM_EXPORT qrm_status qrm_rs_encode_packed(int m, int n, int k, uint64_t message, uint64_t* codeword) {
+    const std::string e = check_code(m, n, k);
+    if (!e.empty()) return fail(QRM_INVALID_INPUT, e);
+    if (n * m > 64) return fail(QRM_INVALID_INPUT, "packed words need n*m <= 64");
+    *codeword = encode_packed(m, n, k, message);
+    return QRM_OK;
+}
+
+QRM_EXPORT qrm_status qrm_ctx_create(int device, const qrm_config* cfg, qrm_ctx** out) {
+    if (!cfg || !out) return fail(QRM_INVALID_INPUT, "null argument");
+    *out = nullptr;
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return fail(QRM_NO_DEVICE, "no CUDA device available");
+    if (device < 0 || device >= ndev) return fail(QRM_INVALID_INPUT, "device index out of range");
+    const std::string ce = check_code(cfg->symbol_bits, cfg->n, cfg->k);
+    if (!ce.empty()) return fail(QRM_INVALID_INPUT, ce);
+    const int nbits = cfg->n * cfg->symbol_bits, kbits = cfg->k * cfg->symbol_bits;
+    if (nbits > kMaxNBits) return fail(QRM_INVALID_INPUT, "the detection path supports codewords up to 64 bits");
+    if (!cfg->key_message) return fail(QRM_INVALID_INPUT, "key message missing");
+    if (cfg->tile_size <= 0 || cfg->tile_size > kWorkingSize) return fail(QRM_INVALID_INPUT, "tile size does not fit image");
+    if (cfg->tile_strategy < 0 || cfg->tile_strategy > 2) return fail(QRM_INVALID_INPUT, "unknown tile strategy");
+    if (cfg->alpha < 0.0) return fail(QRM_INVALID_INPUT, "alpha must be nonnegative");
+    if (!(cfg->fpr_target > 0.0) || !(cfg->fpr_target < 1.0)) return fail(QRM_INVALID_INPUT, "fpr target must be in (0, 1)");
+    if ((cfg->n - cfg->k) / 2 > 8) return fail(QRM_INVALID_INPUT, "detection path supports t <= 8");
+    qrm_status s = set_device(device);
+    if (s != QRM_OK) return s;
+
+    auto c = std::make_unique<qrm_ctx>();
+    c->device = device;
+    c->cfg = *cfg;
+    c->key_message.assign(cfg->key_message, cfg->key_message + kbits);
+    c->cfg.key_message = c->key_message.data();
+    c->m = cfg->symbol_bits;
+    c->n = cfg->n;
+    c->k = cfg->k;
+    c->t = (cfg->n - cfg->k) / 2;
+    c->nbits = nbits;
+    c->kbits = kbits;
+    c->l = cfg->tile_size;
+    c->K = 3 * c->l * c->l;
+    c->K_pad = (c->K + 127) / 128 * 128;
+    QRM_CUDA(cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, device));
+    for (int i = 0; i < kbits; ++i) c->key_msg = (c->key_msg << 1) | (c->key_message[i] & 1);
+    c->key_cw = encode_packed(c->m, c->n, c->k, c->key_msg);
+    c->tau_msg = verify_threshold(kbits, cfg->fpr_target);
+    c->tau_raw = verify_threshold(nbits, cfg->fpr_target);
+    if ((s = rs_tables_for(c->m, c->n, c->k, &c->d_rs)) != QRM_OK) return s;
+    QRM_CUDA(cudaMalloc(&c->d_patterns, static_cast<size_t>(kMaxNBits) * c->K_pad));
+    QRM_CUDA(cudaMalloc(&c->d_colsum, sizeof(int32_t) * kMaxNBits));
+    QRM_LAUNCH(launch_build_patterns(cfg->key_seed, nbits, c->K, c->K_pad, c->d_patterns, c->d_colsum, nullptr));
+    QRM_CUDA(cudaDeviceSynchronize());
+    c->ws.resize(1);
+    *out = c.release();
+    return QRM_OK;
+}
+
+QRM_EXPORT void qrm_ctx_destroy(qrm_ctx* c) {
+    if (!c) return;
+    cudaSetDevice(c->device);
+    for (auto& w : c->ws) w.release();
+    for (auto s : c->streams) cudaStreamDestroy(s);
+    cudaFree(c->d_patterns);
+    cudaFree(c->d_colsum);
+    cudaFree(c->d_records);
+    delete c;
+}
+
+QRM_EXPORT qrm_status qrm_ctx_info(const qrm_ctx* c, uint64_t* key_codeword, uint64_t* key_message, int* tau_msg,
+                                   int* tau_raw) {
+    if (!c) return fail(QRM_INVALID_INPUT, "null context");
+    if (key_codeword) *key_codeword = c->key_cw;
+    if (key_message) *key_message = c->key_msg;
+    if (tau_msg) *tau_msg = c->tau_msg;
+    if (tau_raw) *tau_raw = c->tau_raw;
+    return QRM_OK;
+}
+
+QRM_EXPORT qrm_status qrm_ctx_set_plan(qrm_ctx* c, const qrm_plan* plan) {
+    if (!c || !plan) return fail(QRM_INVALID_INPUT, "null argument");
+    for (int k = 0; k < 3; ++k)
+        if (plan->streams[k] < 1 || plan->minibatch[k] < 1) return fail(QRM_INVALID_INPUT, "plan has an empty stage");
+    c->plan = *plan;
+    return QRM_OK;
+}
+
+QRM_EXPORT qrm_status qrm_detect_device(qrm_ctx* c, const uint8_t* images, int64_t count, int w, int h,
+                                        int64_t stride, uint64_t first_draw, qrm_record* out, void* stream) {
+    qrm_status s = check_uniform(c, images, count, w, h, stride);
+    if (s != QRM_OK) return s;
+    if (count > 0 && !out) return fail(QRM_INVALID_INPUT, "null record buffer");
+    if ((s = set_device(c->device)) != QRM_OK) return s;
+    return detect_uniform(c, c->ws[0], images, count, w, h, stride, first_draw, out, nullptr, nullptr,
+                          as_stream(stream));
+}
+
+QRM_EXPORT qrm_status qrm_probe_decode_kernel(qrm_ctx* c, const uint8_t* images, int64_t count, int w, int h,
+                                              int64_t stride, int reps, double* avg_ms) {
+    qrm_status s = check_uniform(c, images, count, w, h, stride);
+    if (s != QRM_OK) return s;
+    if (reps < 1 || !avg_ms) return fail(QRM_INVALID_INPUT, "bad probe arguments");
+    if ((s = set_device(c->device)) != QRM_OK) return s;
+    if ((s = ensure(c->d_records, c->records_cap, count)) != QRM_OK) return s;
+    QRM_CUDA(cudaEventCreate(&g_probe[0]));
+    QRM_CUDA(cudaEventCreate(&g_probe[1]));
+    double total = 0.0;
+    for (int i = 0; i < reps && s == QRM_OK; ++i) {
+        s = detect_uniform(c, c->ws[0], images, count, w, h, stride, static_cast<uint64_t>(i) * count, c->d_records,
+                           nullptr, nullptr, nullptr);
+        cudaEventSynchronize(g_probe[1]);
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, g_probe[0], g_probe[1]);
+        total += ms;
+    }
+    cudaDeviceSynchronize();
+    cudaEventDestroy(g_probe[0]);
+    cudaEventDestroy(g_probe[1]);
+    g_probe[0] = g_probe[1] = nullptr;
+    if (s != QRM_OK) return s;
+    *avg_ms = total / reps;
+    return QRM_OK;
+}
+
+QRM_EXPORT qrm_status qrm_extract_device(qrm_ctx* c, const uint8_t* images, int64_t count, int w, int h,
+                                         int64_t stride, uint64_t first_draw, double* soft, uint64_t* raw,
+                                         void* stream) {
+    qrm_status s = check_uniform(c, images, count, w, h, stride);
+    if (s != QRM_OK) return s;
+    if ((s = set_device(c->device)) != QRM_OK) return s;
+    if ((s = ensure(c->d_records, c->records_cap, count)) != QRM_OK) return s;
+    return detect_uniform(c, c->ws[0], images, count, w, h, stride, first_draw, c->d_records, soft, raw,
+                          as_stream(stream));
+}
+
+QRM_EXPORT qrm_status qrm_detect_ragged(qrm_ctx* c, const uint8_t* const* images, const int* widths,
+                                        const int* heights, int64_t count, uint64_t first_draw, qrm_record* out) {
+    if (!c) return fail(QRM_INVALID_INPUT, "null context");
+    if (count < 0) return fail(QRM_INVALID_INPUT, "negative image count");
+    if (count == 0) return QRM_OK;
+    if (!images || !widths || !heights || !out) return fail(QRM_INVALID_INPUT, "null argument");
+    qrm_status s = set_device(c->device);
+    if (s != QRM_OK) return s;
+    std::vector<int64_t> off(count + 1, 0);
+    for (int64_t i = 0; i < count; ++i) {
+        if (widths[i] <= 0 || heights[i] <= 0) return fail(QRM_INVALID_INPUT, "image dimensions must be positive");
+        if (!images[i]) return fail(QRM_INVALID_INPUT, "null image pointer");
+        off[i + 1] = off[i] + static_cast<int64_t>(widths[i]) * heights[i] * 3;
+    }
+    Workspace& w = c->ws[0];
+    if ((s = ensure(w.images, w.images_cap, off[count])) != QRM_OK) return s;
+    if ((s = ensure(w.stage, w.stage_cap, count * c->K)) != QRM_OK) return s;
+    if ((s = ensure(w.descs, w.desc_cap, count)) != QRM_OK) return s;
+    if ((s = ensure(c->d_records, c->records_cap, count)) != QRM_OK) return s;
+    for (int64_t i = 0; i < count; ++i)
+        QRM_CUDA(cudaMemcpy(w.images + off[i], images[i], off[i + 1] - off[i], cudaMemcpyHostToDevice));
+    std::vector<GatherDesc> d(count);
+    for (int64_t i = 0; i < count; ++i) {
+        int up, sw, sh, xo, yo, tx, ty;
+        geometry(widths[i], heights[i], up, sw, sh, xo, yo);
+        select_tile(kWorkingSize, kWorkingSize, c->l, c->cfg.tile_strategy, c->cfg.tile_seed,
+                    first_draw + static_cast<uint64_t>(i), tx, ty);
+        d[i] = GatherDesc{w.images + off[i], widths[i], heights[i], up, sw, sh, xo, yo, tx, ty};
+    }
+    QRM_CUDA(cudaMemcpy(w.descs, d.data(), sizeof(GatherDesc) * count, cudaMemcpyHostToDevice));
+    QRM_LAUNCH(launch_gather_windows(w.descs, count, c->l, w.stage, nullptr));
+    WindowSource src{};
+    src.base = w.stage;
+    src.image_stride = c->K;
+    src.pitch = 3 * c->l;
+    src.direct = 0;
+    src.l = c->l;
+    src.strategy = c->cfg.tile_strategy;
+    src.tile_seed = c->cfg.tile_seed;
+    src.first_draw = first_draw;
+    if ((s = run_detect(c, w, src, count, c->d_records, nullptr, nullptr, nullptr)) != QRM_OK) return s;
+    QRM_CUDA(cudaMemcpy(out, c->d_records, sizeof(qrm_record) * count, cudaMemcpyDeviceToHost));
+    return QRM_OK;
+}
+
+QRM_EXPORT qrm_status qrm_detect_host(qrm_ctx* c, const uint8_t* images, int64_t count, int w, int h,
+                                      int64_t stride, uint64_t first_draw, qrm_record* out, const qrm_plan* plan,
+                                      int mode, qrm_host_stats* stats) {
+    qrm_status s = check_uniform(c, images, count, w, h, stride);
+    if (s != QRM_OK) return s;
+    if (count > 0 && !out) return fail(QRM_INVALID_INPUT, "null record buffer");
+    if (mode != 0 && mode != 1) return fail(QRM_INVALID_INPUT, "mode must be 0 (window) or 1 (full image)");
+    if ((s = set_device(c->device)) != QRM_OK) return s;
+    const qrm_plan P = plan ? *plan : c->plan;
+    for (int k = 0; k < 3; ++k)
+        if (P.streams[k] < 1 || P.minibatch[k] < 1) return fail(QRM_INVALID_INPUT, "plan has an empty stage");
+    const int64_t t0 = now_ns();
+    if (count == 0) return QRM_OK;
+
+    // Host buffers must be page-locked and mapped; register them for the call if not.
+    const int64_t in_bytes = (count - 1) * stride + static_cast<int64_t>(w) * h * 3;
+    bool reg_in = false, reg_out = false;
+    cudaPointerAttributes attr{};
+    if (cudaPointerGetAttributes(&attr, images) != cudaSuccess || attr.type != cudaMemoryTypeHost) {
+        cudaGetLastError();
+        QRM_CUDA(cudaHostRegister(const_cast<uint8_t*>(images), in_bytes,
+                                  cudaHostRegisterMapped | cudaHostRegisterReadOnly));
+        reg_in = true;
+    }
+    if (cudaPointerGetAttributes(&attr, out) != cudaSuccess || attr.type != cudaMemoryTypeHost) {
+        cudaGetLastError();
+        QRM_CUDA(cudaHostRegister(out, sizeof(qrm_record) * count, cudaHostRegisterDefault));
+        reg_out = true;
+    }
+    uint8_t* dimg = nullptr;
+    QRM_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&dimg), const_cast<uint8_t*>(images), 0));
+
+    // Streams: [0, s0) transfer, [s0, s0+s1) decode, [s0+s1, s0+s1+s2) correct/return.
+    const int s0 = P.streams[0], s1 = P.streams[1], s2 = P.streams[2];
+    const int nstreams = s0 + s1 + s2;
+    while (static_cast<int>(c->streams.size()) < nstreams) {
+        cudaStream_t st;
+        QRM_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+        c->streams.push_back(st);
+    }
+    const int64_t mb = P.minibatch[1];
+    const int64_t nmb = (count + mb - 1) / mb;
+    // One workspace per decode stream slot (pending lists are per launch).
+    if (static_cast<int>(c->ws.size()) < 1 + s1) c->ws.resize(1 + s1);
+    if ((s = ensure(c->d_records, c->records_cap, count)) != QRM_OK) return s;
+    // Full-image mode: one device image buffer per decode slot.
+    const int64_t img_bytes = static_cast<int64_t>(w) * h * 3;
+    if (mode == 1)
+        for (int j = 0; j < s1; ++j)
+            if ((s = ensure(c->ws[1 + j].images, c->ws[1 + j].images_cap, mb * img_bytes)) != QRM_OK) return s;
+
+    std::vector<cudaEvent_t> ev(4 * nstreams + 3 * nmb);
+    for (auto& e : ev) QRM_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    size_t evi = 0;
+    std::vector<cudaEvent_t> slot_free(s1, nullptr);  // decode slot j reusable after its last finish
+    double h2d = 0.0;
+    int launches0 = static_cast<int>(g_launches.load());
+    for (int64_t b = 0; b < nmb; ++b) {
+        const int64_t first = b * mb;
+        const int64_t cnt = std::min(mb, count - first);
+        cudaStream_t xs = c->streams[b % s0];
+        cudaStream_t ds = c->streams[s0 + b % s1];
+        cudaStream_t cs = c->streams[s0 + s1 + b % s2];
+        const int slot = static_cast<int>(b % s1);
+        Workspace& W = c->ws[1 + slot];
+        const uint8_t* src = dimg + first * stride;
+        int64_t src_stride = stride;
+        if (slot_free[slot]) QRM_CUDA(cudaStreamWaitEvent(xs, slot_free[slot], 0));
+        if (mode == 1) {
+            // stage 0: H2D of the mini-batch's full images on the copy stream
+            QRM_CUDA(cudaMemcpy2DAsync(W.images, img_bytes, images + first * stride, stride, img_bytes, cnt,
+                                       cudaMemcpyHostToDevice, xs));
+            h2d += static_cast<double>(img_bytes) * cnt;
+            src = W.images;
+            src_stride = img_bytes;
+        } else {
+            h2d += static_cast<double>(c->K) * cnt;  // window bytes read over PCIe by the decode kernel
+        }
+        cudaEvent_t e_in = ev[evi++];
+        QRM_CUDA(cudaEventRecord(e_in, xs));
+        QRM_CUDA(cudaStreamWaitEvent(ds, e_in, 0));
+        if (slot_free[slot]) QRM_CUDA(cudaStreamWaitEvent(ds, slot_free[slot], 0));
+        cudaEvent_t e_mid = ev[evi++];
+        // stage 1 (decode) on ds, stage 2 (complete + return) on cs
+        if ((s = detect_uniform(c, W, src, cnt, w, h, src_stride, first_draw + static_cast<uint64_t>(first),
+                                c->d_records + first, nullptr, nullptr, ds, e_mid, cs)) != QRM_OK)
+            return s;
+        QRM_CUDA(cudaMemcpyAsync(out + first, c->d_records + first, sizeof(qrm_record) * cnt, cudaMemcpyDeviceToHost,
+                                 cs));
+        cudaEvent_t e_done = ev[evi++];
+        QRM_CUDA(cudaEventRecord(e_done, cs));
+        slot_free[slot] = e_done;
+    }
+    for (int i = 0; i < nstreams; ++i) QRM_CUDA(cudaStreamSynchronize(c->streams[i]));
+    for (auto& e : ev) cudaEventDestroy(e);
+    if (reg_in) cudaHostUnregister(const_cast<uint8_t*>(images));
+    if (reg_out) cudaHostUnregister(out);
+    if (stats) {
+        stats->wall_ms = static_cast<double>(now_ns() - t0) / 1e6;
+        stats->h2d_bytes = h2d;
+        stats->d2h_bytes = static_cast<double>(sizeof(qrm_record)) * count;
+        stats->minibatches = static_cast<int>(nmb);
+        stats->kernel_launches = static_cast<int>(g_launches.load()) - launches0;
+    }
+    return QRM_OK;
+}
+
+QRM_EXPORT qrm_status qrm_preprocess_host(const uint8_t* image, int w, int h, float* out) {
+    // Full preprocess (transforms.cpp:42-47) on the device: the 256x256 crop is
+    // gathered as one "tile" of size 256 with the fixed strategy.
+    if (!image || !out) return fail(QRM_INVALID_INPUT, "null argument");
+    if (w <= 0 || h <= 0) return fail(QRM_INVALID_INPUT, "image dimensions must be positive");
+    int up, sw, sh, xo, yo;
+    geometry(w, h, up, sw, sh, xo, yo);
+    const int64_t bytes = static_cast<int64_t>(w) * h * 3;
+    const int64_t K = 256 * 256 * 3;
+    uint8_t *dimg = nullptr, *dwin = nullptr;
+    GatherDesc* dd = nullptr;
+    QRM_CUDA(cudaMalloc(&dimg, bytes));
+    QRM_CUDA(cudaMalloc(&dwin, K));
+    QRM_CUDA(cudaMalloc(&dd, sizeof(GatherDesc)));
+    QRM_CUDA(cudaMemcpy(dimg, image, bytes, cudaMemcpyHostToDevice));
+    GatherDesc d{dimg, w, h, up, sw, sh, xo, yo, 0, 0};
+    QRM_CUDA(cudaMemcpy(dd, &d, sizeof d, cudaMemcpyHostToDevice));
+    QRM_LAUNCH(launch_gather_windows(dd, 1, 256, dwin, nullptr));
+    std::vector<uint8_t> win(K);
+    QRM_CUDA(cudaMemcpy(win.data(), dwin, K, cudaMemcpyDeviceToHost));
+    cudaFree(dimg);
+    cudaFree(dwin);
+    cudaFree(dd);
+    for (int64_t i = 0; i < K; ++i) out[i] = static_cast<float>(win[i] / 127.5 - 1.0);  // image.cpp:36
+    return QRM_OK;
+}
+
+QRM_EXPORT qrm_status qrm_rs_decode_packed_device(int m, int n, int k, const uint64_t* words, int64_t count,
+                                                  uint64_t* cw_out, int8_t* nerr_out, int algo, void* stream) {
+    const std::string e = check_code(m, n, k);
+    if (!e.empty()) return fail(QRM_INVALID_INPUT, e);
+    if (n * m > 64) return fail(QRM_INVALID_INPUT, "packed words need n*m <= 64");
+    if (count < 0) return fail(QRM_INVALID_INPUT, "negative count");
+    const int t = (n - k) / 2;
+    if (algo == 0) algo = (t == 1 && n - k <= 3) ? 1 : 2;
+    if (algo == 1 && !(t == 1 && n - k <= 3)) return fail(QRM_INVALID_INPUT, "thread decoder needs t = 1");
+    if (t > 8) return fail(QRM_INVALID_INPUT, "packed warp decoder supports t <= 8");
+    const RsTables* tab;
+    qrm_status s = rs_tables_for(m, n, k, &tab);
+    if (s != QRM_OK) return s;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    QRM_LAUNCH(launch_rs_packed(tab, t, algo, words, count, cw_out, nerr_out, sms, as_stream(stream)));
+    return QRM_OK;
+}
+
+QRM_EXPORT qrm_status qrm_rs_decode_symbols_device(int m, int n, int k, const uint8_t* recv, int64_t count,
+                                                   uint8_t* cw_out, int8_t* nerr_out, void* stream) {
+    const std::string e = check_code(m, n, k);
+    if (!e.empty()) return fail(QRM_INVALID_INPUT, e);
+    if (count < 0) return fail(QRM_INVALID_INPUT, "negative count");
+    const int t = (n - k) / 2;
+    if (t > 16) return fail(QRM_INVALID_INPUT, "symbol decoder supports t <= 16");
+    const RsTables* tab;
+    qrm_status s = rs_tables_for(m, n, k, &tab);
+    if (s != QRM_OK) return s;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    QRM_LAUNCH(launch_rs_symbols(tab, n, t, recv, count, cw_out, nerr_out, sms, as_stream(stream)));
+    return QRM_OK;
+}
+
+// RS stress words for the RS-only benchmark (device): message, received word,
+// injected error count.
+QRM_EXPORT qrm_status qrm_rs_stress_device(int m, int n, int k, uint64_t seed, int64_t count, uint64_t* msg,
+                                           uint64_t* words, int8_t* nerr_true, void* stream) {
+    const std::string e = check_code(m, n, k);
+    if (!e.empty()) return fail(QRM_INVALID_INPUT, e);
+    if (n * m > 64 || n > 32) return fail(QRM_INVALID_INPUT, "stress words need n*m <= 64");
+    const RsTables* tab;
+    qrm_status s = rs_tables_for(m, n, k, &tab);
+    if (s != QRM_OK) return s;
+    auto masks = build_encoder_masks(m, n, k);
+    uint64_t* dm = nullptr;
+    QRM_CUDA(cudaMalloc(&dm, sizeof(uint64_t) * std::max<size_t>(1, masks.size())));
+    QRM_CUDA(cudaMemcpy(dm, masks.data(), sizeof(uint64_t) * masks.size(), cudaMemcpyHostToDevice));
+    QRM_LAUNCH(launch_rs_stress(tab, dm, seed, count, msg, words, nerr_true, as_stream(stream)));
+    QRM_CUDA(cudaStreamSynchronize(as_stream(stream)));
+    cudaFree(dm);
+    return QRM_OK;
+}
+
+QRM_EXPORT qrm_status qrm_patterns_device(uint64_t key_seed, int n_bits, int l, int8_t* out, void* stream) {
+    if (n_bits <= 0 || n_bits > kMaxNBits || l <= 0) return fail(QRM_INVALID_INPUT, "bad pattern geometry");
+    const int K = 3 * l * l;
+    int32_t* cs = nullptr;
+    QRM_CUDA(cudaMalloc(&cs, sizeof(int32_t) * kMaxNBits));
+    int8_t* tmp = nullptr;
+    QRM_CUDA(cudaMalloc(&tmp, static_cast<size_t>(kMaxNBits) * K));
+    QRM_LAUNCH(launch_build_patterns(key_seed, n_bits, K, K, tmp, cs, as_stream(stream)));
+    QRM_CUDA(cudaMemcpyAsync(out, tmp, static_cast<size_t>(n_bits) * K, cudaMemcpyDeviceToDevice, as_stream(stream)));
+    QRM_CUDA(cudaStreamSynchronize(as_stream(stream)));
+    cudaFree(cs);
+    cudaFree(tmp);
+    return QRM_OK;
+}
+
+QRM_EXPORT qrm_status qrm_make_corpus_device(const qrm_config* cfg, uint64_t first_seed, int64_t count, int w, int h,
+                                             int embed, uint8_t* out, void* stream) {
+    if (!cfg) return fail(QRM_INVALID_INPUT, "null config");
+    if (w <= 0 || h <= 0 || count < 0) return fail(QRM_INVALID_INPUT, "bad corpus geometry");
+    float* delta = nullptr;
+    const int l = cfg->tile_size;
+    if (embed) {
+        const std::string ce = check_code(cfg->symbol_bits, cfg->n, cfg->k);
+        if (!ce.empty()) return fail(QRM_INVALID_INPUT, ce);
+        const int nbits = cfg->n * cfg->symbol_bits, kbits = cfg->k * cfg->symbol_bits;
+        if (nbits > 64) return fail(QRM_INVALID_INPUT, "corpus embedding supports codewords up to 64 bits");
+        if (!cfg->key_message) return fail(QRM_INVALID_INPUT, "key message missing");
+        uint64_t msg = 0;
+        for (int i = 0; i < kbits; ++i) msg = (msg << 1) | (cfg->key_message[i] & 1);
+        const uint64_t cw = encode_packed(cfg->symbol_bits, cfg->n, cfg->k, msg);
+        QRM_CUDA(cudaMalloc(&delta, sizeof(float) * 3 * l * l));
+        QRM_LAUNCH(launch_residual(cfg->key_seed, nbits, 3 * l * l, cw, delta, as_stream(stream)));
+    }
+    QRM_LAUNCH(launch_corpus(first_seed, count, w, h, l, embed, static_cast<float>(cfg->alpha), delta, out,
+                             as_stream(stream)));
+    if (delta) {
+        QRM_CUDA(cudaStreamSynchronize(as_stream(stream)));
+        cudaFree(delta);
+    }
+    return QRM_OK;
+}
+
+QRM_EXPORT qrm_status qrm_allocate_streams(int stages, const double* time, const double* memory, double b0,
+                                           int global_batch, int budget, double m_cap, double eps, int stall_cap,
+                                           int* streams_out, int* mb_out, double* bottleneck) {
+    if (stages <= 0 || !time || !memory || !streams_out || !mb_out || !bottleneck)
+        return fail(QRM_INVALID_INPUT, "bad arguments");
+    sched::Profile p;
+    p.b0 = b0;
+    p.time.assign(time, time + stages);
+    p.memory.assign(memory, memory + stages);
+    sched::Plan plan;
+    std::string err;
+    const int rc = sched::allocate_streams(p, global_batch, budget, m_cap, eps, stall_cap, plan, err);
+    if (rc) return fail(static_cast<qrm_status>(rc), err);
+    for (int k = 0; k < stages; ++k) {
+        streams_out[k] = plan.streams[k];
+        mb_out[k] = plan.minibatch[k];
+    }
+    *bottleneck = plan.bottleneck;
+    return QRM_OK;
+}
+
+QRM_EXPORT qrm_status qrm_lpt_schedule(int ntasks, const int* ids, const double* lat, const double* mem,
+                                       const int* units, int S, double lambda, double m_cap, int b_min, int B,
+                                       int capacity, int* p_stream, int* p_id, int* p_units, double* p_lat,
+                                       double* p_mem, int* p_mb, int* n_pieces, double* loads, int* m_unit) {
+    std::vector<sched::Task> tasks(ntasks);
+    for (int i = 0; i < ntasks; ++i) {
+        tasks[i].id = ids[i];
+        tasks[i].latency = lat[i];
+        tasks[i].memory = mem[i];
+        tasks[i].units = units[i];
+    }
+    sched::Schedule out;
+    std::string err;
+    const int rc = sched::lpt_schedule(tasks, S, lambda, m_cap, b_min, B, out, err);
+    if (rc) return fail(static_cast<qrm_status>(rc), err);
+    int c = 0;
+    for (int st = 0; st < S; ++st) {
+        loads[st] = out.loads[st];
+        for (const auto& t : out.streams[st]) {
+            if (c < capacity) {
+                p_stream[c] = st;
+                p_id[c] = t.id;
+                p_units[c] = t.units;
+                p_lat[c] = t.latency;
+                p_mem[c] = t.memory;
+                p_mb[c] = t.mb;
+            }
+            ++c;
+        }
+    }
+    *n_pieces = c;
+    *m_unit = out.m_unit;
+    return QRM_OK;
+}
+
+QRM_EXPORT qrm_status qrm_warmup_profile(qrm_ctx* c, const uint8_t* images, int64_t count, int w, int h,
+                                         int64_t stride, int iters, int b0, double* time, double* memory) {
+    // warmup_profile (sim.cpp:240-288) for the device stages: medians of
+    // cudaEvent-timed runs of transfer / decode / correct+return at batch b0.
+    qrm_status s = check_uniform(c, images, count, w, h, stride);
+    if (s != QRM_OK) return s;
+    if (iters < 1) return fail(QRM_INVALID_INPUT, "need at least one warm-up iteration");
+    if (count == 0) return fail(QRM_INVALID_INPUT, "warm-up needs at least one image");
+    if ((s = set_device(c->device)) != QRM_OK) return s;
+    b0 = static_cast<int>(std::min<int64_t>(std::max(1, b0), count));
+    const int64_t img_bytes = static_cast<int64_t>(w) * h * 3;
+    Workspace& W = c->ws[0];
+    if ((s = ensure(W.images, W.images_cap, b0 * img_bytes)) != QRM_OK) return s;
+    if ((s = ensure(c->d_records, c->records_cap, b0)) != QRM_OK) return s;
+    std::vector<qrm_record> host(b0);
+    cudaStream_t st = nullptr;
+    cudaEvent_t a, b;
+    QRM_CUDA(cudaEventCreate(&a));
+    QRM_CUDA(cudaEventCreate(&b));
+    auto timed = [&](auto&& body) -> double {
+        cudaEventRecord(a, st);
+        body();
+        cudaEventRecord(b, st);
+        cudaEventSynchronize(b);
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, a, b);
+        return ms;
+    };
+    std::vector<double> t0v, t1v, t2v;
+    for (int i = 0; i < iters; ++i) {
+        t0v.push_back(timed([&] {
+            cudaMemcpy2DAsync(W.images, img_bytes, images, stride, img_bytes, b0, cudaMemcpyHostToDevice, st);
+        }));
+        t1v.push_back(timed([&] {
+            detect_uniform(c, W, W.images, b0, w, h, img_bytes, 0, c->d_records, nullptr, nullptr, st);
+        }));
+        t2v.push_back(timed([&] {
+            cudaMemcpyAsync(host.data(), c->d_records, sizeof(qrm_record) * b0, cudaMemcpyDeviceToHost, st);
+        }));
+    }
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    auto med = [](std::vector<double> v) {
+        std::sort(v.begin(), v.end());
+        double x = v[v.size() / 2];
+        if (v.size() % 2 == 0) x = 0.5 * (x + v[v.size() / 2 - 1]);
+        return std::max(x, 1e-6);
+    };
+    time[0] = med(t0v);
+    time[1] = med(t1v);
+    time[2] = med(t2v);
+    memory[0] = static_cast<double>(img_bytes);
+    memory[1] = static_cast<double>(c->K + sizeof(PendingEntry));
+    memory[2] = static_cast<double>(sizeof(qrm_record));
+    QRM_CUDA(cudaGetLastError());
+    return QRM_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,199 @@
+// Device-side building blocks shared by the sm_100a kernels.
+//
+//  * counter RNG (reference include/qrmark/rng.hpp:13-39), usable on host and device
+//  * tile selection (reference src/tiling.cpp:23-47)
+//  * thin PTX wrappers: mbarrier, cp.async, proxy fences, tcgen05 (TMEM alloc,
+//    MMA, commit, ld) — written for sm_100a only.
+#pragma once
+
+#include <cstdint>
+
+#include "qrm_types.h"
+
+#define QRM_HD __host__ __device__ __forceinline__
+#define QRM_D __device__ __forceinline__
+
+namespace qrm {
+
+// ---------------------------------------------------------------- rng ----
+constexpr uint64_t kGolden = 0x9e3779b97f4a7c15ULL;
+
+QRM_HD uint64_t mix64(uint64_t x) {
+    x ^= x >> 30;
+    x *= 0xbf58476d1ce4e5b9ULL;
+    x ^= x >> 27;
+    x *= 0x94d049bb133111ebULL;
+    x ^= x >> 31;
+    return x;
+}
+
+QRM_HD uint64_t rng_word(uint64_t seed, uint64_t stream, uint64_t ctr) {
+    const uint64_t key = mix64(seed + kGolden * (stream + 1));
+    return mix64(key ^ (ctr * 0xd6e8feb86659fd93ULL) ^ (ctr >> 32));
+}
+
+QRM_HD uint64_t mulhi64(uint64_t a, uint64_t b) {
+#ifdef __CUDA_ARCH__
+    return __umul64hi(a, b);
+#else
+    return static_cast<uint64_t>((static_cast<unsigned __int128>(a) * b) >> 64);
+#endif
+}
+
+QRM_HD uint64_t rng_below(uint64_t seed, uint64_t stream, uint64_t ctr, uint64_t bound) {
+    return mulhi64(rng_word(seed, stream, ctr), bound);
+}
+
+QRM_HD double rng_unit(uint64_t seed, uint64_t stream, uint64_t ctr) {
+    return static_cast<double>(rng_word(seed, stream, ctr) >> 11) * 0x1.0p-53;
+}
+
+// Tile origin inside the w x h working image (tiling.cpp:23-47).
+// strategy: 0 random, 1 random_grid, 2 fixed.
+QRM_HD void select_tile(int w, int h, int l, int strategy, uint64_t seed, uint64_t draw, int& x, int& y) {
+    if (strategy == QRM_TILE_FIXED) {
+        x = 0;
+        y = 0;
+    } else if (strategy == QRM_TILE_RANDOM) {
+        x = static_cast<int>(rng_below(seed, 2 * draw, 0, static_cast<uint64_t>(w - l) + 1));
+        y = static_cast<int>(rng_below(seed, 2 * draw + 1, 0, static_cast<uint64_t>(h - l) + 1));
+    } else {
+        const uint64_t cols = static_cast<uint64_t>(w / l), rows = static_cast<uint64_t>(h / l);
+        const uint64_t cell = rng_below(seed, draw, 0, cols * rows);
+        x = static_cast<int>(cell % cols) * l;
+        y = static_cast<int>(cell / cols) * l;
+    }
+}
+
+#ifdef __CUDACC__
+// --------------------------------------------------------------- smem ----
+QRM_D uint32_t smem_u32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
+
+// ----------------------------------------------------------- mbarrier ----
+QRM_D void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+
+QRM_D void mbar_fence_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+
+QRM_D void mbar_arrive(uint64_t* bar) {
+    asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.shared::cta.b64 st, [%0];\n\t}" ::"r"(smem_u32(bar))
+                 : "memory");
+}
+
+QRM_D bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+
+QRM_D void mbar_wait(uint64_t* bar, uint32_t parity) {
+    while (!mbar_try_wait(bar, parity)) {
+    }
+}
+
+// ----------------------------------------------------------- cp.async ----
+// 16-byte global->shared copy through L2 only (.cg); src_bytes < 16 zero-fills.
+QRM_D void cp_async16(uint32_t dst_smem, const void* src, uint32_t src_bytes = 16) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst_smem), "l"(src), "r"(src_bytes)
+                 : "memory");
+}
+QRM_D void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+QRM_D void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+// Make generic-proxy shared-memory writes visible to the async proxy (tcgen05.mma).
+QRM_D void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+// ------------------------------------------------------------ tcgen05 ----
+template <uint32_t kCols>
+QRM_D void tmem_alloc(uint32_t* dst_smem_slot) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(dst_smem_slot)),
+                 "n"(kCols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+}
+
+template <uint32_t kCols>
+QRM_D void tmem_dealloc(uint32_t taddr) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "n"(kCols) : "memory");
+}
+
+QRM_D void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+QRM_D void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+// D[tmem] (+)= A[smem] * B[smem], kind::i8 (u8 x s8 -> s32).
+QRM_D void umma_i8(uint32_t tmem_d, uint64_t desc_a, uint64_t desc_b, uint32_t idesc, uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(desc_a), "l"(desc_b), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+
+// D[tmem] (+)= A[smem] * B[smem], kind::f16 (bf16 x bf16 -> f32).
+QRM_D void umma_bf16(uint32_t tmem_d, uint64_t desc_a, uint64_t desc_b, uint32_t idesc, uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(desc_a), "l"(desc_b), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+
+// Arrive (once) on an mbarrier when all previously issued tcgen05.mma of this
+// thread have completed. Implies tcgen05.fence::before_thread_sync.
+QRM_D void umma_commit(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+                 : "memory");
+}
+
+// 32 lanes x 16 consecutive 32-bit columns -> 16 registers per thread.
+QRM_D void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr)
+        : "memory");
+}
+QRM_D void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+// Shared-memory matrix descriptor: K-major operand in the 128-byte swizzle
+// canonical layout (rows of 128 B, 8-row groups 1024 B apart).
+QRM_D uint64_t sw128_kmajor_desc(uint32_t smem_addr) {
+    uint64_t d = 0;
+    d |= static_cast<uint64_t>((smem_addr >> 4) & 0x3FFF);  // start address
+    d |= static_cast<uint64_t>(1) << 16;                    // LBO (ignored for swizzled K-major)
+    d |= static_cast<uint64_t>(1024 >> 4) << 32;            // SBO: 8-row group stride
+    d |= static_cast<uint64_t>(1) << 46;                    // descriptor version (sm_100)
+    d |= static_cast<uint64_t>(2) << 61;                    // SWIZZLE_128B
+    return d;
+}
+
+// Instruction descriptor (kind::i8): D s32, A u8, B s8, both K-major.
+QRM_HD uint32_t idesc_i8_u8s8(int M, int N) {
+    return (2u << 4) | (0u << 7) | (1u << 10) | (static_cast<uint32_t>(N >> 3) << 17) |
+           (static_cast<uint32_t>(M >> 4) << 24);
+}
+
+// Instruction descriptor (kind::f16): D f32, A bf16, B bf16, both K-major.
+QRM_HD uint32_t idesc_bf16_f32(int M, int N) {
+    return (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(N >> 3) << 17) |
+           (static_cast<uint32_t>(M >> 4) << 24);
+}
+
+// Byte offset of 16-byte chunk `c` of row `r` inside a 128B-swizzled K-major tile.
+QRM_HD uint32_t sw128_offset(uint32_t r, uint32_t c) { return r * 128u + ((c ^ (r & 7u)) << 4); }
+#endif  // __CUDACC__
+
+}  // namespace qrm

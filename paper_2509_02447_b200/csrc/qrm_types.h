@@ -1,0 +1,79 @@
+// Internal host/device types of the B200 detection path (not part of the ABI).
+#pragma once
+
+#include <cstdint>
+
+#include "qrmark_gpu.h"
+
+namespace qrm {
+
+constexpr int kWorkingSize = 256;  // transforms.hpp:11
+constexpr int kMaxNBits = 64;      // codeword bits handled by the fused detect path
+constexpr uint8_t kRecPending = 0xFF;
+
+// GF(2^m) tables + GRS parity structure of an (n, k) evaluation code with
+// X_i = alpha^i (rs.cpp:52-63). Lives in device global memory; kernels stage
+// it into shared memory.
+struct RsTables {
+    int32_t m, n, k, t, r, q1;  // r = n - k, q1 = 2^m - 1
+    int32_t packed_ok;          // n*m <= 64
+    int32_t nmask;              // r*m syndrome-bit masks (packed words)
+    uint8_t exp2[512];          // alpha^i for i in [0, 2*q1), no modulo needed
+    uint8_t log[256];           // log_alpha(v), v in [1, q1]
+    uint8_t logv[256];          // log of the GRS column multipliers v_i = 1/prod_{l!=i}(X_i - X_l)
+    uint64_t synd_mask[64];     // packed-word syndrome bits: S_j bit e = parity(word & synd_mask[j*m+e])
+};
+
+// One pending detection (tie resolution and/or general-t RS correction).
+struct PendingEntry {
+    int64_t image;
+    uint64_t tie_mask;  // bit i set: correlation of pattern i was exactly zero
+};
+
+// Window addressing of the decode kernels. direct != 0: the tile window is
+// read straight from the raw image (uniform batch, crop offset + per-image
+// tile origin from the counter RNG). direct == 0: windows were staged
+// contiguously (3 l^2 bytes each) by the gather kernel.
+struct WindowSource {
+    const uint8_t* base;
+    int64_t image_stride;
+    int32_t pitch;      // bytes per image row (direct) / 3l (staged)
+    int32_t x_off;      // centre-crop offset, pixels (direct only)
+    int32_t y_off;
+    int32_t direct;
+    int32_t strategy;
+    int32_t l;
+    uint64_t tile_seed;
+    uint64_t first_draw;
+};
+
+struct GatherDesc {
+    const uint8_t* img;  // image base (device or mapped host)
+    int32_t w, h;        // source size
+    int32_t upscale;
+    int32_t sw, sh;      // virtual resized size
+    int32_t x_off, y_off;
+    int32_t tx, ty;      // tile origin in the 256 x 256 working image
+};
+
+struct DetectParams {
+    WindowSource src;
+    int64_t count;
+    int32_t K;          // 3 l^2 correlation length
+    int32_t K_pad;      // rounded up to the 128-byte pipeline chunk
+    int32_t nbits;      // n*m
+    int32_t kbits;      // k*m
+    int32_t tau_msg, tau_raw;
+    int32_t fuse_t1;    // epilogue may run the t=1 RS decoder itself
+    uint64_t key_cw, key_msg;
+    const int8_t* patterns;   // [64][K_pad] s8, rows >= nbits zero
+    const int32_t* colsum;    // [64] sum_px P_i[px]
+    const RsTables* rs;
+    qrm_record* out;
+    double* soft;             // nullable, [count][nbits]
+    uint64_t* raw_out;        // nullable, [count]
+    int32_t* pending_count;
+    PendingEntry* pending;    // capacity = count
+};
+
+}  // namespace qrm

@@ -1,0 +1,162 @@
+"""GPU Reed-Solomon decoders vs the reference bw_decode (rs.cpp:188-196), bit-exact.
+
+Mirrors the reference's own RS tests (proj/tests/test_rs.cpp) and adds large
+differential runs: every GPU output (codeword, errors_corrected, failure) must
+equal the compiled reference / the C oracle on the same received words.
+"""
+import numpy as np
+import pytest
+
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+
+def _random_msgs(rng, count, kb):
+    hi = rng.integers(0, 1 << 32, size=count, dtype=np.uint64)
+    lo = rng.integers(0, 1 << 32, size=count, dtype=np.uint64)
+    w = (hi << np.uint64(32)) | lo
+    if kb < 64:
+        w &= np.uint64((1 << kb) - 1)
+    return w
+
+
+def _corrupt(rng, words, m, n, nerr):
+    """Flip `nerr[i]` distinct symbols of word i by a nonzero xor."""
+    out = words.copy()
+    q1 = (1 << m) - 1
+    for i in range(words.size):
+        pos = rng.choice(n, size=int(nerr[i]), replace=False)
+        for p in pos:
+            out[i] ^= np.uint64(int(rng.integers(1, q1 + 1)) << (m * (n - 1 - int(p))))
+    return out
+
+
+def _encode_all(qrm, code, msgs):
+    return np.array([qrm.rs_encode_packed(code, int(x)) for x in msgs], dtype=np.uint64)
+
+
+def _gpu_decode(qrm, cuda, code, words, algo):
+    w = cuda.tensor(words.view(np.int64), device="cuda")
+    cw, ne = qrm.bw_decode_packed(code, w, algo=algo)
+    cuda.cuda.synchronize()
+    return cw.cpu().numpy().view(np.uint64), ne.cpu().numpy()
+
+
+@pytest.mark.parametrize("profile", ["gf16-15-12", "gf256-dynamic"])
+@pytest.mark.parametrize("algo", [1, 2])
+def test_packed_matches_reference(qrm, cuda, orc, profile, algo):
+    code = qrm.resolve_profile(profile, 48)
+    rng = np.random.default_rng(7 + algo)
+    N = 6000
+    msgs = _random_msgs(rng, N, code.message_bits())
+    cws = _encode_all(qrm, code, msgs)
+    nerr = rng.integers(0, 4, size=N)
+    words = _corrupt(rng, cws, code.m, code.n, nerr)
+    # plus fully random words (mostly uncorrectable)
+    words = np.concatenate([words, _random_msgs(rng, 2000, code.codeword_bits())])
+    cw_g, ne_g = _gpu_decode(qrm, cuda, code, words, algo)
+    cw_o, ne_o = orc.bw_decode_packed(code.m, code.n, code.k, words)
+    assert np.array_equal(ne_g, ne_o)
+    ok = ne_o >= 0
+    assert np.array_equal(cw_g[ok], cw_o[ok])
+    # e <= t always decodes back to the transmitted codeword
+    small = np.arange(N)[nerr <= code.t]
+    assert np.array_equal(cw_g[small], cws[small])
+    assert np.array_equal(ne_g[small], nerr[small])
+
+
+def test_exhaustive_single_symbol_corruption(qrm, cuda):
+    """test_rs.cpp:93-114: 10 messages x 15 positions x 15 wrong values."""
+    code = qrm.resolve_profile("gf16-15-12")
+    rng = np.random.default_rng(23)
+    msgs = _random_msgs(rng, 10, 48)
+    words, expect = [], []
+    for m_ in msgs:
+        cw = qrm.rs_encode_packed(code, int(m_))
+        for pos in range(15):
+            sh = 4 * (14 - pos)
+            cur = (cw >> sh) & 0xF
+            for wrong in range(16):
+                if wrong != cur:
+                    words.append(cw ^ ((cur ^ wrong) << sh))
+                    expect.append(cw)
+    words = np.array(words, dtype=np.uint64)
+    for algo in (1, 2):
+        cw_g, ne_g = _gpu_decode(qrm, cuda, code, words, algo)
+        assert (ne_g == 1).all()
+        assert np.array_equal(cw_g, np.array(expect, dtype=np.uint64))
+        assert np.array_equal(cw_g >> np.uint64(12), np.repeat(msgs, 225))
+
+
+def test_t2_symbols_match_reference(qrm, cuda, ref):
+    """(12,8) over GF(256), t=2 (test_rs.cpp:116-134) plus beyond-capacity words."""
+    code = qrm.CodeParams.make(8, 12, 8)
+    rng = np.random.default_rng(24)
+    N = 3000
+    rows = []
+    for i in range(N):
+        msg = rng.integers(0, 256, size=8)
+        bits = np.array([(int(v) >> (7 - b)) & 1 for v in msg for b in range(8)], np.uint8)
+        cwb = ref.rs_encode(8, 12, 8, bits)
+        sym = np.array([oracle.bits_to_word(cwb[8 * j:8 * j + 8]) for j in range(12)], np.uint8)
+        e = int(rng.integers(0, 5))
+        for p in rng.choice(12, size=e, replace=False):
+            sym[p] ^= np.uint8(rng.integers(1, 256))
+        rows.append(sym)
+    recv = np.stack(rows)
+    cw_r, ne_r = ref.bw_decode_symbols(8, 12, 8, recv)
+    cw_g, ne_g = qrm.bw_decode_symbols(code, cuda.tensor(recv, device="cuda"))
+    cw_g, ne_g = cw_g.cpu().numpy(), ne_g.cpu().numpy()
+    assert np.array_equal(ne_g, ne_r)
+    ok = ne_r >= 0
+    assert np.array_equal(cw_g[ok], cw_r[ok])
+
+
+@pytest.mark.parametrize("mnk", [(8, 30, 20), (4, 15, 9), (8, 100, 68)])
+def test_general_t_symbols_match_reference(qrm, cuda, ref, mnk):
+    m, n, k = mnk
+    code = qrm.CodeParams.make(m, n, k)
+    t = code.t
+    rng = np.random.default_rng(n * 7 + k)
+    N = 400 if n < 100 else 60
+    rows = []
+    for _ in range(N):
+        msg = rng.integers(0, 1 << m, size=k)
+        bits = np.array([(int(v) >> (m - 1 - b)) & 1 for v in msg for b in range(m)], np.uint8)
+        cwb = ref.rs_encode(m, n, k, bits)
+        sym = np.array([oracle.bits_to_word(cwb[m * j:m * j + m]) for j in range(n)], np.uint8)
+        e = int(rng.integers(0, t + 3))
+        for p in rng.choice(n, size=e, replace=False):
+            sym[p] ^= np.uint8(rng.integers(1, 1 << m))
+        rows.append(sym)
+    recv = np.stack(rows)
+    cw_r, ne_r = ref.bw_decode_symbols(m, n, k, recv)
+    cw_g, ne_g = qrm.bw_decode_symbols(code, cuda.tensor(recv, device="cuda"))
+    cw_g, ne_g = cw_g.cpu().numpy(), ne_g.cpu().numpy()
+    assert np.array_equal(ne_g, ne_r)
+    ok = ne_r >= 0
+    assert np.array_equal(cw_g[ok], cw_r[ok])
+
+
+def test_stress_10m_properties(qrm, cuda, orc):
+    """Config 4: 10M gf16-15-12 words with injected errors; e <= t decode exactly,
+    and a 100K slice (all classes) matches the oracle bit-exactly."""
+    code = qrm.resolve_profile("gf16-15-12")
+    N = 10_000_000
+    msg, words, ne_true = qrm.rs_stress_words(code, 2026, N)
+    for algo in (1, 2):
+        cw, ne = qrm.bw_decode_packed(code, words, algo=algo)
+        cuda.cuda.synchronize()
+        small = ne_true <= code.t
+        assert bool((ne[small] == ne_true[small]).all())
+        assert bool(((cw[small] >> 12) == msg[small]).all())
+        big = ~small
+        frac = float(big.float().mean().item()) if hasattr(big, "float") else 0.0
+        assert 0.08 < frac < 0.12
+        sl = slice(0, 100_000)
+        w_h = words[sl].cpu().numpy().view(np.uint64)
+        cw_o, ne_o = orc.bw_decode_packed(code.m, code.n, code.k, w_h)
+        assert np.array_equal(ne[sl].cpu().numpy(), ne_o)
+        okm = ne_o >= 0
+        assert np.array_equal(cw[sl].cpu().numpy().view(np.uint64)[okm], cw_o[okm])
