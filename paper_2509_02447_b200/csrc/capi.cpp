@@ -31,7 +31,7 @@
 #include "sched_host.hpp"
 
 namespace qrm {
-cudaError_t launch_corr_detect(const DetectParams& p, cudaStream_t st);
+cudaError_t launch_corr_detect(const DetectParams& p, int sm_count, cudaStream_t st);
 cudaError_t launch_detect_finish(const DetectParams& p, int tmax, int sm_count, cudaStream_t st);
 cudaError_t launch_gather_windows(const GatherDesc* descs, int64_t count, int l, uint8_t* out, cudaStream_t st);
 cudaError_t launch_rs_packed(const RsTables* tab, int t, int algo, const uint64_t* words, int64_t count, uint64_t* cw,
@@ -216,7 +216,7 @@ qrm_status run_detect(qrm_ctx* c, Workspace& w, const WindowSource& src, int64_t
     p.src = src;
     QRM_CUDA(cudaMemsetAsync(w.pending_count, 0, sizeof(int32_t), st));
     if (g_probe[0]) QRM_CUDA(cudaEventRecord(g_probe[0], st));
-    QRM_LAUNCH(launch_corr_detect(p, st));
+    QRM_LAUNCH(launch_corr_detect(p, c->sms, st));
     if (g_probe[1]) QRM_CUDA(cudaEventRecord(g_probe[1], st));
     cudaStream_t fs = st;
     if (mid_event && finish_stream) {

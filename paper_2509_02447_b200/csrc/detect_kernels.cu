@@ -42,6 +42,8 @@ constexpr int kCorrProducers = 128;
 constexpr int kCorrThreads = 160;
 constexpr int kCorrLag = 3;  // cp.async groups in flight per producer thread
 
+constexpr int kRedStride = kCorrN + 4;  // int32 words per reduction row (padded: conflict-free v4 access)
+
 struct CorrSmem {
     uint64_t full[kCorrStages];
     uint64_t empty[kCorrStages];
@@ -49,9 +51,48 @@ struct CorrSmem {
     uint32_t tmem_base;
     int32_t colsum[kCorrN];
     RsSmem rs;
+    // Split-K partials from the cluster: [rank][row within my 128/S rows][kRedStride]
+    alignas(16) int32_t red[kCorrM * kRedStride];
 };
 
 constexpr size_t kCorrSmemBytes = 1024 /*align slack*/ + kCorrStages * kCorrStageBytes + sizeof(CorrSmem);
+
+// Epilogue for one image (one TMEM lane): S = 2 D - 255 colsum, harden, pack,
+// and — t = 1 code, no exact-zero correlation — RS-correct + verify in place.
+__device__ __forceinline__ void finish_image(const DetectParams& p, const CorrSmem& sm, int64_t img,
+                                             const uint32_t (&acc)[kCorrN]) {
+    const int nb = p.nbits;
+    uint64_t raw = 0, tmask = 0;
+    const double inv = 1.0 / (255.0 * static_cast<double>(p.K));
+#pragma unroll
+    for (int i = 0; i < kCorrN; ++i) {
+        if (i < nb) {
+            const int S = 2 * static_cast<int>(acc[i]) - 255 * sm.colsum[i];
+            raw |= static_cast<uint64_t>(S > 0) << (nb - 1 - i);
+            tmask |= static_cast<uint64_t>(S == 0) << i;
+            if (p.soft) p.soft[img * nb + i] = static_cast<double>(S) * inv;
+        }
+    }
+    if (p.raw_out) p.raw_out[img] = raw;
+    qrm_record rec;
+    if (tmask == 0 && p.fuse_t1) {
+        uint64_t cw = 0;
+        const int nerr = rs_t1_packed(sm.rs, raw, cw);
+        make_record(rec, raw, nerr, cw, nb, p.kbits, p.key_cw, p.key_msg, p.tau_msg, p.tau_raw, 0);
+    } else {
+        rec.raw = raw;
+        rec.msg = 0;
+        rec.status = kRecPending;
+        rec.errors = 0;
+        rec.matches = 0;
+        rec.verified = 0;
+        rec.ties = static_cast<uint8_t>(__popcll(tmask));
+        rec.reserved[0] = rec.reserved[1] = rec.reserved[2] = 0;
+        const int slot = atomicAdd(p.pending_count, 1);
+        p.pending[slot] = PendingEntry{img, tmask};
+    }
+    p.out[img] = rec;
+}
 
 __device__ __forceinline__ const uint8_t* window_base(const WindowSource& s, int64_t img, int K) {
     if (!s.direct) return s.base + img * static_cast<int64_t>(K);
@@ -62,6 +103,10 @@ __device__ __forceinline__ const uint8_t* window_base(const WindowSource& s, int
            static_cast<int64_t>(s.x_off + tx) * 3;
 }
 
+// Launched as clusters of S = 1, 2 or 4 CTAs along K (split-K): CTA r of a
+// cluster accumulates K chunks [r K/S, (r+1) K/S) of the same 128 images in its
+// own TMEM, pushes the partial rows owned by each peer into the peer's shared
+// memory (DSMEM), and after one cluster barrier each CTA finishes 128/S images.
 __global__ void __launch_bounds__(kCorrThreads, 1) corr_detect_kernel(const __grid_constant__ DetectParams p) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* ring = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -70,8 +115,12 @@ __global__ void __launch_bounds__(kCorrThreads, 1) corr_detect_kernel(const __gr
     const int tid = threadIdx.x;
     const int warp = tid >> 5;
     const int lane = tid & 31;
-    const int64_t m0 = static_cast<int64_t>(blockIdx.x) * kCorrM;
-    const int kchunks = p.K_pad / kCorrKC;
+    const uint32_t S = cluster_nctarank();  // 1 without a cluster launch
+    const uint32_t rank = cluster_ctarank();
+    const int64_t m0 = static_cast<int64_t>(blockIdx.x / S) * kCorrM;
+    const int kc_total = p.K_pad / kCorrKC;
+    const int kc_begin = static_cast<int>(static_cast<int64_t>(kc_total) * rank / S);
+    const int kchunks = static_cast<int>(static_cast<int64_t>(kc_total) * (rank + 1) / S) - kc_begin;
 
     if (warp == 4) tmem_alloc<kCorrN>(&sm.tmem_base);
     if (tid == 0) {
@@ -88,6 +137,7 @@ __global__ void __launch_bounds__(kCorrThreads, 1) corr_detect_kernel(const __gr
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = sm.tmem_base;
+    const int rows_per = kCorrM / static_cast<int>(S);
 
     if (warp < 4) {
         // ------------------------------------------------------ producer --
@@ -109,7 +159,7 @@ __global__ void __launch_bounds__(kCorrThreads, 1) corr_detect_kernel(const __gr
             mbar_wait(&sm.empty[s], ((it / kCorrStages) & 1) ^ 1);
             const uint32_t a_s = ring_u32 + s * kCorrStageBytes;
             const uint32_t b_s = a_s + kCorrABytes;
-            const int kbyte = it * kCorrKC + c * 16;
+            const int kbyte = (kc_begin + it) * kCorrKC + c * 16;
             if (kbyte < p.K) {
                 const int trow = kbyte / row_bytes;
                 const int64_t off = static_cast<int64_t>(trow) * pitch + (kbyte - trow * row_bytes);
@@ -148,39 +198,19 @@ __global__ void __launch_bounds__(kCorrThreads, 1) corr_detect_kernel(const __gr
         tmem_ld_wait();
         tc_fence_before();
 
-        const int64_t img = m0 + warp * 32 + lane;
-        if (img < p.count) {
-            const int nb = p.nbits;
-            uint64_t raw = 0, tmask = 0;
-            const double inv = 1.0 / (255.0 * static_cast<double>(p.K));
+        const int row = warp * 32 + lane;
+        if (S == 1) {
+            const int64_t img = m0 + row;
+            if (img < p.count) finish_image(p, sm, img, acc);
+        } else {
+            // push this partial row to its owner CTA: slot `rank`, local row
+            const uint32_t owner = static_cast<uint32_t>(row / rows_per);
+            const uint32_t local = static_cast<uint32_t>(row % rows_per);
+            const uint32_t dst = map_to_rank(
+                smem_u32(&sm.red[(rank * rows_per + local) * kRedStride]), owner);
 #pragma unroll
-            for (int i = 0; i < kCorrN; ++i) {
-                if (i < nb) {
-                    const int S = 2 * static_cast<int>(acc[i]) - 255 * sm.colsum[i];
-                    raw |= static_cast<uint64_t>(S > 0) << (nb - 1 - i);
-                    tmask |= static_cast<uint64_t>(S == 0) << i;
-                    if (p.soft) p.soft[img * nb + i] = static_cast<double>(S) * inv;
-                }
-            }
-            if (p.raw_out) p.raw_out[img] = raw;
-            qrm_record rec;
-            if (tmask == 0 && p.fuse_t1) {
-                uint64_t cw = 0;
-                const int nerr = rs_t1_packed(sm.rs, raw, cw);
-                make_record(rec, raw, nerr, cw, nb, p.kbits, p.key_cw, p.key_msg, p.tau_msg, p.tau_raw, 0);
-            } else {
-                rec.raw = raw;
-                rec.msg = 0;
-                rec.status = kRecPending;
-                rec.errors = 0;
-                rec.matches = 0;
-                rec.verified = 0;
-                rec.ties = static_cast<uint8_t>(__popcll(tmask));
-                rec.reserved[0] = rec.reserved[1] = rec.reserved[2] = 0;
-                const int slot = atomicAdd(p.pending_count, 1);
-                p.pending[slot] = PendingEntry{img, tmask};
-            }
-            p.out[img] = rec;
+            for (int q = 0; q < kCorrN / 4; ++q)
+                st_cluster_v4(dst + 16 * q, acc[4 * q], acc[4 * q + 1], acc[4 * q + 2], acc[4 * q + 3]);
         }
     } else if (warp == 4) {
         // ------------------------------------------------------ MMA issuer --
@@ -202,6 +232,27 @@ __global__ void __launch_bounds__(kCorrThreads, 1) corr_detect_kernel(const __gr
             umma_commit(&sm.accum_full);
         }
         __syncwarp();
+    }
+    if (S > 1) {
+        cluster_sync_all();  // every partial row has landed in its owner's smem
+        if (tid < rows_per) {
+            uint32_t acc[kCorrN];
+#pragma unroll
+            for (int i = 0; i < kCorrN; ++i) acc[i] = 0;
+            for (uint32_t s = 0; s < S; ++s) {
+                const int4* src = reinterpret_cast<const int4*>(&sm.red[(s * rows_per + tid) * kRedStride]);
+#pragma unroll
+                for (int q = 0; q < kCorrN / 4; ++q) {
+                    const int4 v = src[q];
+                    acc[4 * q] += v.x;
+                    acc[4 * q + 1] += v.y;
+                    acc[4 * q + 2] += v.z;
+                    acc[4 * q + 3] += v.w;
+                }
+            }
+            const int64_t img = m0 + static_cast<int64_t>(rank) * rows_per + tid;
+            if (img < p.count) finish_image(p, sm, img, acc);
+        }
     }
     __syncthreads();
     if (warp == 4) {
@@ -330,7 +381,7 @@ __global__ void gather_windows_kernel(const GatherDesc* __restrict__ descs, int6
 // ---------------------------------------------------------------- launch --
 static inline bool ok(cudaError_t e) { return e == cudaSuccess; }
 
-cudaError_t launch_corr_detect(const DetectParams& p, cudaStream_t st) {
+cudaError_t launch_corr_detect(const DetectParams& p, int sm_count, cudaStream_t st) {
     static bool configured = false;
     if (!configured) {
         cudaError_t e = cudaFuncSetAttribute(corr_detect_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -339,8 +390,25 @@ cudaError_t launch_corr_detect(const DetectParams& p, cudaStream_t st) {
         configured = true;
     }
     const int64_t tiles = (p.count + kCorrM - 1) / kCorrM;
-    corr_detect_kernel<<<static_cast<unsigned>(tiles), kCorrThreads, kCorrSmemBytes, st>>>(p);
-    return cudaGetLastError();
+    if (tiles == 0) return cudaSuccess;
+    // Split K over a cluster when there are too few 128-image tiles to give
+    // every SM a CTA (one CTA per SM: the 6-stage ring uses ~180 KB of smem).
+    const int sms = sm_count > 0 ? sm_count : 148;
+    unsigned S = 1;
+    while (S < 4 && tiles * S * 2 <= sms && (p.K_pad / kCorrKC) >= static_cast<int>(8 * S * 2)) S *= 2;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(static_cast<unsigned>(tiles) * S);
+    cfg.blockDim = dim3(kCorrThreads);
+    cfg.dynamicSmemBytes = kCorrSmemBytes;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = S;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, corr_detect_kernel, p);
 }
 
 cudaError_t launch_detect_finish(const DetectParams& p, int tmax, int sm_count, cudaStream_t st) {

@@ -25,6 +25,35 @@ __global__ void __launch_bounds__(256) rs_t1_packed_kernel(const RsTables* __res
     }
 }
 
+// Vectorised form: each thread decodes 4 consecutive words (two 16-byte
+// loads issued before any compute, so each thread keeps 32 B in flight);
+// requires 16-byte aligned word arrays and 4-byte aligned nerr.
+__global__ void __launch_bounds__(256) rs_t1_packed_x4_kernel(const RsTables* __restrict__ g,
+                                                             const ulonglong2* __restrict__ words, int64_t groups,
+                                                             ulonglong2* __restrict__ cw_out,
+                                                             uint32_t* __restrict__ nerr_out) {
+    __shared__ RsSmem T;
+    rs_stage_tables(T, g, threadIdx.x, blockDim.x);
+    __syncthreads();
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < groups; i += stride) {
+        const ulonglong2 a = __ldcs(words + 2 * i);
+        const ulonglong2 b = __ldcs(words + 2 * i + 1);
+        uint64_t w[4] = {a.x, a.y, b.x, b.y}, c[4];
+        uint32_t ne = 0;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            uint64_t cw = 0;
+            const int e = rs_t1_packed(T, w[j], cw);
+            c[j] = e >= 0 ? cw : 0ull;
+            ne |= (static_cast<uint32_t>(e) & 0xFFu) << (8 * j);
+        }
+        __stcs(cw_out + 2 * i, make_ulonglong2(c[0], c[1]));
+        __stcs(cw_out + 2 * i + 1, make_ulonglong2(c[2], c[3]));
+        __stcs(nerr_out + i, ne);
+    }
+}
+
 // One codeword per warp, packed words (n <= 32 symbols).
 template <int TMAX>
 __global__ void __launch_bounds__(256) rs_warp_packed_kernel(const RsTables* __restrict__ g,
@@ -128,10 +157,25 @@ cudaError_t launch_rs_packed(const RsTables* tab, int t, int algo, const uint64_
     if (count <= 0) return cudaSuccess;
     const int sms = sm_count > 0 ? sm_count : 148;
     if (algo == 1) {
-        int64_t blocks = (count + 255) / 256;
-        const int64_t cap = static_cast<int64_t>(sms) * 8;
-        if (blocks > cap) blocks = cap;
-        rs_t1_packed_kernel<<<static_cast<unsigned>(blocks), 256, 0, st>>>(tab, words, count, cw, nerr);
+        const bool vec = (reinterpret_cast<uintptr_t>(words) % 16 == 0) && (reinterpret_cast<uintptr_t>(cw) % 16 == 0) &&
+                         (reinterpret_cast<uintptr_t>(nerr) % 4 == 0);
+        const int64_t groups = vec ? count / 4 : 0;
+        if (groups > 0) {
+            int64_t blocks = (groups + 255) / 256;
+            const int64_t cap = static_cast<int64_t>(sms) * 16;
+            if (blocks > cap) blocks = cap;
+            rs_t1_packed_x4_kernel<<<static_cast<unsigned>(blocks), 256, 0, st>>>(
+                tab, reinterpret_cast<const ulonglong2*>(words), groups, reinterpret_cast<ulonglong2*>(cw),
+                reinterpret_cast<uint32_t*>(nerr));
+        }
+        const int64_t done = groups * 4, rest = count - done;
+        if (rest > 0) {
+            int64_t blocks = (rest + 255) / 256;
+            const int64_t cap = static_cast<int64_t>(sms) * 8;
+            if (blocks > cap) blocks = cap;
+            rs_t1_packed_kernel<<<static_cast<unsigned>(blocks), 256, 0, st>>>(tab, words + done, rest, cw + done,
+                                                                               nerr + done);
+        }
     } else {
         int64_t blocks = (count + 7) / 8;
         const int64_t cap = static_cast<int64_t>(sms) * 16;
