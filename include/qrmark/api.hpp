@@ -1,0 +1,428 @@
+// qrmark/api.hpp — the reference's C++ detection API (proj/include/qrmark/*.hpp),
+// re-declared for the B200-native implementation so existing callers compile
+// and link unchanged (drop-in). One consolidated header; the per-module
+// headers qrmark/{errors,rng,gf,rs,image,transforms,tiling,stego,detect,sched,sim}.hpp
+// include it.
+//
+// Implementation: libqrmark_b200.so (csrc/dropin.cpp) over the C-ABI in
+// qrmark_gpu.h. The hot path — detect_batch / detect_one / bw_decode /
+// SpreadSpectrumCodec::extract / preprocess — runs on the GPU (no CPU
+// fallback; a missing device raises CudaUnavailable). Field arithmetic,
+// bit packing, the planners (Algorithms 1 and 2) and other host bookkeeping
+// are plain C++ as in the reference.
+//
+// Out of scope (not on the north-star path): attack
+// transforms, PPM I/O, PSNR, JSON/CLI, and the discrete-event simulator.
+#pragma once
+
+#include <array>
+#include <cstdint>
+#include <functional>
+#include <mutex>
+#include <optional>
+#include <span>
+#include <stdexcept>
+#include <string>
+#include <unordered_map>
+#include <utility>
+#include <vector>
+
+namespace qrmark {
+
+// ------------------------------------------------------------- errors.hpp
+class InvalidInput : public std::invalid_argument {
+public:
+    explicit InvalidInput(const std::string& w) : std::invalid_argument(w) {}
+};
+class DivisionByZero : public std::domain_error {
+public:
+    explicit DivisionByZero(const std::string& w) : std::domain_error(w) {}
+};
+class InfeasibleConfig : public std::runtime_error {
+public:
+    explicit InfeasibleConfig(const std::string& w) : std::runtime_error(w) {}
+};
+// Raised when the CUDA device / library cannot run a compute call.
+class CudaUnavailable : public std::runtime_error {
+public:
+    explicit CudaUnavailable(const std::string& w) : std::runtime_error(w) {}
+};
+
+// ---------------------------------------------------------------- rng.hpp
+inline constexpr uint64_t kGolden = 0x9e3779b97f4a7c15ULL;
+constexpr uint64_t mix64(uint64_t x) {
+    x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    x = (x ^ (x >> 27)) * 0x94d049bb133111ebULL;
+    return x ^ (x >> 31);
+}
+constexpr uint64_t rng_word(uint64_t seed, uint64_t stream, uint64_t counter) {
+    return mix64(mix64(seed + kGolden * (stream + 1)) ^ (counter * 0xd6e8feb86659fd93ULL) ^ (counter >> 32));
+}
+constexpr uint64_t rng_below(uint64_t seed, uint64_t stream, uint64_t counter, uint64_t bound) {
+    return static_cast<uint64_t>((static_cast<unsigned __int128>(rng_word(seed, stream, counter)) * bound) >> 64);
+}
+constexpr double rng_unit(uint64_t seed, uint64_t stream, uint64_t counter) {
+    return static_cast<double>(rng_word(seed, stream, counter) >> 11) * 0x1.0p-53;
+}
+class CounterRng {
+public:
+    CounterRng(uint64_t seed, uint64_t stream) : seed_(seed), stream_(stream) {}
+    uint64_t next() { return rng_word(seed_, stream_, ctr_++); }
+    uint64_t below(uint64_t bound) { return rng_below(seed_, stream_, ctr_++, bound); }
+    double unit() { return rng_unit(seed_, stream_, ctr_++); }
+
+private:
+    uint64_t seed_, stream_, ctr_ = 0;
+};
+
+// ----------------------------------------------------------------- gf.hpp
+class FieldSpec {
+public:
+    static const FieldSpec& gf16();   // x^4 + x + 1
+    static const FieldSpec& gf256();  // x^8 + x^4 + x^3 + x^2 + 1
+    int bits() const { return m_; }
+    int order() const { return order_; }
+    uint32_t primitive_poly() const { return poly_; }
+    uint16_t add(uint16_t a, uint16_t b) const;
+    uint16_t mul(uint16_t a, uint16_t b) const;
+    uint16_t inv(uint16_t a) const;
+    uint16_t div(uint16_t a, uint16_t b) const;
+    uint16_t pow(uint16_t a, uint64_t e) const;
+    uint16_t alpha_pow(uint32_t i) const { return exp_[i % (order_ - 1)]; }
+    bool operator==(const FieldSpec& o) const { return this == &o; }
+
+private:
+    FieldSpec(int m, uint32_t poly);
+    void check(uint16_t v) const;
+    int m_;
+    uint32_t poly_;
+    int order_;
+    std::vector<uint16_t> exp_, log_;
+};
+
+struct FieldElement {
+    uint16_t value = 0;
+    const FieldSpec* spec = nullptr;
+    FieldElement() = default;
+    FieldElement(uint16_t v, const FieldSpec& s) : value(v), spec(&s) {}
+    friend FieldElement operator+(FieldElement a, FieldElement b);
+    friend FieldElement operator*(FieldElement a, FieldElement b);
+    friend FieldElement operator/(FieldElement a, FieldElement b);
+    friend bool operator==(FieldElement a, FieldElement b) { return a.value == b.value && a.spec == b.spec; }
+};
+
+class Poly {
+public:
+    explicit Poly(const FieldSpec& spec) : spec_(&spec) {}
+    Poly(const FieldSpec& spec, std::vector<uint16_t> coeffs);
+    static Poly zero(const FieldSpec& spec) { return Poly(spec); }
+    static Poly constant(const FieldSpec& spec, uint16_t c) { return Poly(spec, {c}); }
+    const FieldSpec& spec() const { return *spec_; }
+    bool is_zero() const { return c_.empty(); }
+    int degree() const { return static_cast<int>(c_.size()) - 1; }
+    std::span<const uint16_t> coeffs() const { return c_; }
+    uint16_t coeff(size_t i) const { return i < c_.size() ? c_[i] : 0; }
+    uint16_t eval(uint16_t x) const;
+    friend Poly operator+(const Poly& a, const Poly& b);
+    friend Poly operator*(const Poly& a, const Poly& b);
+    Poly scaled(uint16_t s) const;
+    static std::pair<Poly, Poly> divmod(const Poly& num, const Poly& den);
+    bool operator==(const Poly& o) const { return spec_ == o.spec_ && c_ == o.c_; }
+
+private:
+    const FieldSpec* spec_;
+    std::vector<uint16_t> c_;
+};
+
+Poly lagrange_interpolate(const FieldSpec& spec, std::span<const std::pair<uint16_t, uint16_t>> points);
+
+// ----------------------------------------------------------------- rs.hpp
+using BitVec = std::vector<uint8_t>;
+std::vector<uint16_t> bits_to_symbols(const BitVec& bits, int m);
+BitVec symbols_to_bits(std::span<const uint16_t> symbols, int m);
+std::string bits_to_hex(const BitVec& bits);
+BitVec hex_to_bits(const std::string& hex, size_t n_bits);
+
+struct CodeParams {
+    const FieldSpec* field = nullptr;
+    int n = 0, k = 0, t = 0;
+    std::vector<uint16_t> eval_points;
+    static CodeParams make(const FieldSpec& field, int n, int k);
+    int message_bits() const { return k * field->bits(); }
+    int codeword_bits() const { return n * field->bits(); }
+};
+CodeParams resolve_profile(const std::string& name, int payload_bits = 48);
+
+struct DecodeResult {
+    BitVec message;
+    BitVec codeword;
+    int errors_corrected;
+};
+BitVec rs_encode(const BitVec& message, const CodeParams& params);
+// GPU bounded-distance decoder, bit-exact with the reference Berlekamp-Welch.
+std::optional<DecodeResult> bw_decode(const BitVec& received, const CodeParams& params);
+// Batched form (one launch for all words) — the way to decode at scale.
+std::vector<std::optional<DecodeResult>> bw_decode_batch(std::span<const BitVec> received, const CodeParams& params);
+double rs_aware_loss(const BitVec& predicted, const BitVec& target, const CodeParams& params);
+double bit_accuracy(const BitVec& a, const BitVec& b);
+double word_accuracy(const std::vector<BitVec>& decoded, const std::vector<BitVec>& truth);
+
+// -------------------------------------------------------------- image.hpp
+enum class PixelForm : uint8_t { byte, normalized };
+struct ImageBuffer {
+    int width = 0, height = 0, channels = 3;
+    PixelForm form = PixelForm::byte;
+    std::vector<uint8_t> bytes;
+    std::vector<float> values;
+    static ImageBuffer make_byte(int w, int h);
+    static ImageBuffer make_normalized(int w, int h);
+    size_t sample_count() const { return static_cast<size_t>(width) * height * channels; }
+    size_t index(int x, int y, int c) const { return (static_cast<size_t>(y) * width + x) * channels + c; }
+    uint8_t at8(int x, int y, int c) const { return bytes[index(x, y, c)]; }
+    uint8_t& at8(int x, int y, int c) { return bytes[index(x, y, c)]; }
+    float atf(int x, int y, int c) const { return values[index(x, y, c)]; }
+    float& atf(int x, int y, int c) { return values[index(x, y, c)]; }
+};
+ImageBuffer normalize(const ImageBuffer& img);    // GPU
+ImageBuffer denormalize(const ImageBuffer& img);  // host (input generation)
+ImageBuffer resize_bilinear(const ImageBuffer& img, int out_w, int out_h);  // GPU
+ImageBuffer center_crop(const ImageBuffer& img, int side_w, int side_h);    // GPU (byte) / copy (normalized)
+ImageBuffer synthetic_image(uint64_t seed, int w, int h);                   // GPU corpus generator
+
+// --------------------------------------------------------- transforms.hpp
+inline constexpr int kWorkingSize = 256;
+ImageBuffer preprocess(const ImageBuffer& img);        // GPU
+ImageBuffer preprocess_fused(const ImageBuffer& img);  // GPU (same kernel: the fused form)
+
+// ------------------------------------------------------------- tiling.hpp
+enum class TileStrategy { random, random_grid, fixed };
+TileStrategy parse_tile_strategy(const std::string& name);
+std::string tile_strategy_name(TileStrategy s);
+struct TileSpec {
+    int size = 64;
+    TileStrategy strategy = TileStrategy::random_grid;
+    uint64_t seed = 0;
+};
+struct TileRef {
+    int x = 0, y = 0, size = 0;
+    bool operator==(const TileRef&) const = default;
+};
+TileRef select_tile(int width, int height, const TileSpec& spec, uint64_t draw_index = 0);
+TileRef select_tile(const ImageBuffer& img, const TileSpec& spec, uint64_t draw_index = 0);
+std::vector<TileRef> grid_cells(int width, int height, int l);
+ImageBuffer extract_tile(const ImageBuffer& img, const TileRef& tile);
+
+// -------------------------------------------------------------- stego.hpp
+struct WatermarkKey {
+    uint64_t seed = 1;
+    int n_bits = 60;
+    double alpha = 0.04;
+};
+struct SoftBits {
+    std::vector<double> values;
+};
+BitVec harden(const SoftBits& soft);
+
+class WatermarkCodec {
+public:
+    virtual ~WatermarkCodec() = default;
+    virtual int tile_size() const = 0;
+    virtual int payload_bits() const = 0;
+    virtual ImageBuffer embed(const ImageBuffer& tile, const BitVec& bits) const = 0;
+    virtual SoftBits extract(const ImageBuffer& tile) const = 0;
+};
+
+// Spread-spectrum codec; patterns live on the GPU. extract() replays the
+// reference's double summation on the device (bit-identical soft values).
+class SpreadSpectrumCodec : public WatermarkCodec {
+public:
+    SpreadSpectrumCodec(const WatermarkKey& key, int tile_size);
+    int tile_size() const override { return tile_size_; }
+    int payload_bits() const override { return key_.n_bits; }
+    const WatermarkKey& key() const { return key_; }
+    ImageBuffer embed(const ImageBuffer& tile, const BitVec& bits) const override;
+    SoftBits extract(const ImageBuffer& tile) const override;
+    std::vector<float> residual(const BitVec& bits) const;
+    double pattern_correlation(int i, int j) const;
+
+private:
+    size_t samples() const { return static_cast<size_t>(tile_size_) * tile_size_ * 3; }
+    WatermarkKey key_;
+    int tile_size_;
+    std::vector<int8_t> patterns_;  // host copy of the device planes (for residual/correlation)
+};
+void embed_image_grid(ImageBuffer& normalized_img, const SpreadSpectrumCodec& codec, const BitVec& bits);
+ImageBuffer embed(const ImageBuffer& tile, const BitVec& bits, const WatermarkKey& key);
+SoftBits extract(const ImageBuffer& tile, const WatermarkKey& key);
+
+// -------------------------------------------------------------- sched.hpp
+struct StageProfile {
+    double b0 = 1.0;
+    std::vector<double> time, memory, prep;
+    std::vector<std::string> names;
+    int stages() const { return static_cast<int>(time.size()); }
+    double prep_of(int k) const { return k < static_cast<int>(prep.size()) ? prep[k] : 0.0; }
+    void validate() const;
+};
+struct StreamPlan {
+    std::vector<int> streams, minibatch;
+    double bottleneck = 0.0;
+    int total_streams() const;
+};
+double stage_time(const StageProfile& profile, int k, int s_k, int m_k);
+bool mem_ok(std::span<const int> s, std::span<const int> m, std::span<const double> u, double m_cap);
+StreamPlan allocate_streams(const StageProfile& profile, int global_batch, int stream_budget, double m_cap,
+                            double epsilon, int stall_cap);
+struct Task {
+    int id = 0, tile_size = 0;
+    double latency = 0.0, memory = 0.0;
+    int units = 1, mb = 0;
+};
+struct StreamSchedule {
+    std::vector<std::vector<Task>> streams;
+    std::vector<double> loads;
+    int m_unit = 1;
+    double makespan() const;
+    double total_latency() const;
+};
+class TileSizePredictor {
+public:
+    virtual ~TileSizePredictor() = default;
+    virtual int select_tile_size(const ImageBuffer& img) const = 0;
+};
+class ConstantTilePredictor : public TileSizePredictor {
+public:
+    explicit ConstantTilePredictor(int size) : size_(size) {}
+    int select_tile_size(const ImageBuffer&) const override { return size_; }
+
+private:
+    int size_;
+};
+enum class PipelineMode { detect, embed };
+struct WarmupStats {
+    int reference_tile = 64;
+    double detect_latency = 0.0, detect_memory = 0.0, embed_latency = 0.0, embed_memory = 0.0;
+    double latency_for(PipelineMode mode, int tile) const;
+    double memory_for(PipelineMode mode, int tile) const;
+};
+std::vector<Task> build_tasks(std::span<const ImageBuffer> images, const TileSizePredictor& predictor,
+                              const WarmupStats& stats, double b0, PipelineMode mode);
+StreamSchedule lpt_schedule(std::vector<Task> tasks, int stream_count, double lambda, double m_cap, int b_min,
+                            int global_batch);
+
+// ------------------------------------------------------------- detect.hpp
+struct CacheConfig {
+    bool enabled = true;
+    size_t capacity = 4096;
+    uint64_t stale_after = 1u << 20;
+};
+struct DetectionConfig {
+    CodeParams code;
+    TileSpec tile;
+    WatermarkKey key;
+    BitVec key_message;
+    int rs_workers = 32;
+    double fpr_target = 1e-6;
+    CacheConfig cache;
+    static DetectionConfig make(const CodeParams& code, const TileSpec& tile, uint64_t key_seed, double alpha,
+                                BitVec key_message);
+};
+struct StageLatencies {
+    int64_t preprocess_ns = 0, extract_ns = 0, correct_ns = 0;
+};
+struct DetectionRecord {
+    size_t image_index = 0;
+    BitVec raw_bits;
+    std::optional<BitVec> corrected;
+    int errors_corrected = 0;
+    double bit_acc = 0.0;
+    bool verified = false;
+    bool cache_hit = false;
+    StageLatencies stage_ns;
+    std::string error;
+};
+bool semantic_equal(const DetectionRecord& a, const DetectionRecord& b);
+int verify_threshold(int n_bits, double fpr_target);
+bool verify(const BitVec& a, const BitVec& b, double fpr_target);
+
+// The codebook (detect.cpp:86-128), transparent: misses decode on the GPU.
+class CorrectionCache {
+public:
+    explicit CorrectionCache(const CacheConfig& cfg) : cfg_(cfg) {}
+    std::pair<std::optional<DecodeResult>, bool> correct(const BitVec& raw, const CodeParams& params);
+    size_t size() const;
+    uint64_t hits() const { return hits_; }
+    uint64_t lookups() const { return lookups_; }
+
+private:
+    struct Entry {
+        std::optional<DecodeResult> result;
+        uint64_t last_access = 0;
+    };
+    void evict_locked();
+    CacheConfig cfg_;
+    mutable std::mutex mu_;
+    std::unordered_map<std::string, Entry> map_;
+    uint64_t tick_ = 0, hits_ = 0, lookups_ = 0;
+};
+
+struct GpuContext;  // owns the qrm_ctx of the C-ABI
+
+class DetectionContext {
+public:
+    explicit DetectionContext(const DetectionConfig& cfg, int device = 0);
+    ~DetectionContext();
+    DetectionContext(const DetectionContext&) = delete;
+    DetectionContext& operator=(const DetectionContext&) = delete;
+    const DetectionConfig& config() const { return cfg_; }
+    const SpreadSpectrumCodec& codec() const { return codec_; }
+    const BitVec& key_codeword() const { return key_codeword_; }
+    CorrectionCache& cache() { return cache_; }
+    DetectionRecord detect_one(const ImageBuffer& img, uint64_t draw_index);
+    // Batch entry used by detect_batch: records for images with draw_index first_draw + i.
+    std::vector<DetectionRecord> detect_many(std::span<const ImageBuffer> images, uint64_t first_draw,
+                                             const StreamPlan* plan = nullptr);
+    GpuContext* gpu() { return gpu_; }
+
+private:
+    DetectionConfig cfg_;
+    SpreadSpectrumCodec codec_;
+    BitVec key_codeword_;
+    int tau_message_, tau_raw_;
+    CorrectionCache cache_;
+    GpuContext* gpu_;
+};
+DetectionRecord detect_one(const ImageBuffer& img, const DetectionConfig& cfg);
+
+struct SyntheticStageLoad {
+    int64_t preprocess_ns = 0, extract_ns = 0, correct_ns = 0;
+};
+struct DeskReport {
+    int64_t wall_ns = 0;
+    std::array<int64_t, 3> stage_busy_ns{0, 0, 0};
+    std::array<int, 3> stage_workers{1, 1, 1};
+    size_t items = 0;
+};
+// The CUDA-stream pipeline: plan->streams are the per-stage stream counts of
+// the transfer / decode / correct stages, plan->minibatch their mini-batch.
+std::vector<DetectionRecord> detect_batch(std::span<const ImageBuffer> images, const DetectionConfig& cfg,
+                                          const StreamPlan* plan = nullptr, const SyntheticStageLoad* load = nullptr,
+                                          DeskReport* report = nullptr);
+
+// ---------------------------------------------------------------- sim.hpp
+struct StageBench {
+    std::string name;
+    std::function<void()> run_batch;
+    double mem_per_sample = 0.0;
+    double prep_share = 0.0;
+};
+StageProfile measure_stages(std::span<StageBench> stages, int warmup_iters, double baseline_batch,
+                            const std::function<int64_t()>& now_ns);
+// cudaEvent-timed warm-up of the device stages (transfer / decode / correct).
+StageProfile warmup_profile(std::span<const ImageBuffer> images, int warmup_iters, const DetectionConfig& cfg);
+std::pair<std::vector<DetectionRecord>, DeskReport> run_desk(const StreamPlan& plan,
+                                                             std::span<const ImageBuffer> images,
+                                                             const DetectionConfig& cfg,
+                                                             const SyntheticStageLoad* load = nullptr);
+
+}  // namespace qrmark

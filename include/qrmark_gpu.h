@@ -128,7 +128,9 @@ QRM_EXPORT qrm_status qrm_detect_device(qrm_ctx* ctx, const uint8_t* images, int
  * CUDA-stream executor that replaces detect_batch's thread pools and bounded
  * queues). plan == NULL uses the context's current plan (qrm_ctx_set_plan).
  * mode 0: window-only transfer (the tile window is read from mapped pinned host
- * memory by the decode kernel); mode 1: full-image H2D copies. Host images are
+ * memory by the decode kernel); mode 1: full-image H2D copies; mode 2: staged
+ * window transfer (a host worker pool copies each image's l x l window into
+ * pinned staging, one contiguous H2D per mini-batch). Host images are
  * registered (page-locked) for the call if they are not pinned already. */
 QRM_EXPORT qrm_status qrm_detect_host(qrm_ctx* ctx, const uint8_t* images, int64_t count, int w, int h,
                                       int64_t image_stride, uint64_t first_draw, qrm_record* out,

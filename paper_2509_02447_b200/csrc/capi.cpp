@@ -28,6 +28,7 @@
 #include "qrm_device.cuh"
 #include "qrm_types.h"
 #include "qrmark_gpu.h"
+#include "host_pool.hpp"
 #include "sched_host.hpp"
 
 namespace qrm {
@@ -125,7 +126,12 @@ struct Workspace {
     int64_t desc_cap = 0;
     uint8_t* images = nullptr;  // full-image H2D buffer (host pipeline, mode 1)
     int64_t images_cap = 0;
+    uint8_t* host_stage = nullptr;  // pinned window staging (host pipeline, mode 2)
+    int64_t host_stage_cap = 0;
+    cudaEvent_t host_stage_free = nullptr;  // H2D out of host_stage finished
     void release() {
+        if (host_stage) cudaFreeHost(host_stage);
+        if (host_stage_free) cudaEventDestroy(host_stage_free);
         cudaFree(pending_count);
         cudaFree(pending);
         cudaFree(stage);
@@ -153,6 +159,7 @@ struct qrm_ctx {
     std::vector<Workspace> ws;  // [0]: device API; [1..]: host pipeline slots
     std::vector<cudaStream_t> streams;
     qrm_plan plan{{1, 2, 1}, {4096, 4096, 4096}};
+    std::unique_ptr<HostPool> pool;  // window staging workers (host pipeline, mode 2)
 };
 
 namespace {
@@ -500,7 +507,8 @@ QRM_EXPORT qrm_status qrm_detect_host(qrm_ctx* c, const uint8_t* images, int64_t
     qrm_status s = check_uniform(c, images, count, w, h, stride);
     if (s != QRM_OK) return s;
     if (count > 0 && !out) return fail(QRM_INVALID_INPUT, "null record buffer");
-    if (mode != 0 && mode != 1) return fail(QRM_INVALID_INPUT, "mode must be 0 (window) or 1 (full image)");
+    if (mode < 0 || mode > 2)
+        return fail(QRM_INVALID_INPUT, "mode must be 0 (mapped window), 1 (full image) or 2 (staged window)");
     if ((s = set_device(c->device)) != QRM_OK) return s;
     const qrm_plan P = plan ? *plan : c->plan;
     for (int k = 0; k < 3; ++k)
@@ -541,9 +549,29 @@ QRM_EXPORT qrm_status qrm_detect_host(qrm_ctx* c, const uint8_t* images, int64_t
     if ((s = ensure(c->d_records, c->records_cap, count)) != QRM_OK) return s;
     // Full-image mode: one device image buffer per decode slot.
     const int64_t img_bytes = static_cast<int64_t>(w) * h * 3;
+    int up, sw, sh, xo, yo;
+    geometry(w, h, up, sw, sh, xo, yo);
+    if (mode == 2 && up) mode = 1;  // upscaled inputs need the device bilinear gather
     if (mode == 1)
         for (int j = 0; j < s1; ++j)
             if ((s = ensure(c->ws[1 + j].images, c->ws[1 + j].images_cap, mb * img_bytes)) != QRM_OK) return s;
+    if (mode == 2) {
+        if (!c->pool) {
+            const unsigned hc = std::thread::hardware_concurrency();
+            c->pool = std::make_unique<HostPool>(static_cast<int>(std::max(1u, std::min(hc ? hc - 1 : 1u, 31u))));
+        }
+        for (int j = 0; j < s1; ++j) {
+            Workspace& W = c->ws[1 + j];
+            if ((s = ensure(W.stage, W.stage_cap, mb * c->K)) != QRM_OK) return s;
+            if (W.host_stage_cap < mb * c->K) {
+                if (W.host_stage) cudaFreeHost(W.host_stage);
+                W.host_stage = nullptr;
+                QRM_CUDA(cudaHostAlloc(&W.host_stage, mb * c->K, cudaHostAllocDefault));
+                W.host_stage_cap = mb * c->K;
+            }
+            if (!W.host_stage_free) QRM_CUDA(cudaEventCreateWithFlags(&W.host_stage_free, cudaEventDisableTiming));
+        }
+    }
 
     std::vector<cudaEvent_t> ev(4 * nstreams + 3 * nmb);
     for (auto& e : ev) QRM_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
@@ -562,6 +590,49 @@ QRM_EXPORT qrm_status qrm_detect_host(qrm_ctx* c, const uint8_t* images, int64_t
         const uint8_t* src = dimg + first * stride;
         int64_t src_stride = stride;
         if (slot_free[slot]) QRM_CUDA(cudaStreamWaitEvent(xs, slot_free[slot], 0));
+        if (mode == 2) {
+            // stage 0 (CPU part): copy each image's l x l window into pinned
+            // staging with the worker pool, then one contiguous H2D.
+            if (slot_free[slot]) QRM_CUDA(cudaEventSynchronize(slot_free[slot]));
+            uint8_t* hs = W.host_stage;
+            const int l = c->l, rowb = 3 * l, pitch = 3 * w;
+            const int K = c->K;
+            const auto& cfg = c->cfg;
+            c->pool->parallel_for(cnt, 64, [&](int64_t i0, int64_t i1) {
+                for (int64_t i = i0; i < i1; ++i) {
+                    int tx, ty;
+                    select_tile(kWorkingSize, kWorkingSize, l, cfg.tile_strategy, cfg.tile_seed,
+                                first_draw + static_cast<uint64_t>(first + i), tx, ty);
+                    const uint8_t* src0 = images + (first + i) * stride + static_cast<int64_t>(yo + ty) * pitch +
+                                          static_cast<int64_t>(xo + tx) * 3;
+                    uint8_t* dst = hs + i * K;
+                    for (int r = 0; r < l; ++r) std::memcpy(dst + r * rowb, src0 + static_cast<int64_t>(r) * pitch, rowb);
+                }
+            });
+            QRM_CUDA(cudaMemcpyAsync(W.stage, hs, cnt * K, cudaMemcpyHostToDevice, xs));
+            h2d += static_cast<double>(K) * cnt;
+            cudaEvent_t e_in = ev[evi++];
+            QRM_CUDA(cudaEventRecord(e_in, xs));
+            QRM_CUDA(cudaStreamWaitEvent(ds, e_in, 0));
+            WindowSource ws{};
+            ws.base = W.stage;
+            ws.image_stride = K;
+            ws.pitch = rowb;
+            ws.direct = 0;
+            ws.l = l;
+            ws.strategy = cfg.tile_strategy;
+            ws.tile_seed = cfg.tile_seed;
+            ws.first_draw = first_draw + static_cast<uint64_t>(first);
+            cudaEvent_t e_mid = ev[evi++];
+            if ((s = run_detect(c, W, ws, cnt, c->d_records + first, nullptr, nullptr, ds, e_mid, cs)) != QRM_OK)
+                return s;
+            QRM_CUDA(cudaMemcpyAsync(out + first, c->d_records + first, sizeof(qrm_record) * cnt,
+                                     cudaMemcpyDeviceToHost, cs));
+            cudaEvent_t e_done = ev[evi++];
+            QRM_CUDA(cudaEventRecord(e_done, cs));
+            slot_free[slot] = e_done;
+            continue;
+        }
         if (mode == 1) {
             // stage 0: H2D of the mini-batch's full images on the copy stream
             QRM_CUDA(cudaMemcpy2DAsync(W.images, img_bytes, images + first * stride, stride, img_bytes, cnt,

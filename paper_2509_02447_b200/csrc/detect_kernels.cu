@@ -40,7 +40,6 @@ constexpr int kCorrBBytes = kCorrN * kCorrKC;  // 8 KiB
 constexpr int kCorrStageBytes = kCorrABytes + kCorrBBytes;
 constexpr int kCorrProducers = 128;
 constexpr int kCorrThreads = 160;
-constexpr int kCorrLag = 3;  // cp.async groups in flight per producer thread
 
 constexpr int kRedStride = kCorrN + 4;  // int32 words per reduction row (padded: conflict-free v4 access)
 
@@ -91,7 +90,7 @@ __device__ __forceinline__ void finish_image(const DetectParams& p, const CorrSm
         const int slot = atomicAdd(p.pending_count, 1);
         p.pending[slot] = PendingEntry{img, tmask};
     }
-    p.out[img] = rec;
+    store_record(p.out + img, rec);
 }
 
 __device__ __forceinline__ const uint8_t* window_base(const WindowSource& s, int64_t img, int K) {
@@ -172,17 +171,13 @@ __global__ void __launch_bounds__(kCorrThreads, 1) corr_detect_kernel(const __gr
                 const int n = rb + 16 * j;
                 cp_async16(b_s + sw128_offset(n, c), p.patterns + static_cast<int64_t>(n) * p.K_pad + kbyte);
             }
-            cp_async_commit();
-            if (it >= kCorrLag) {
-                cp_async_wait<kCorrLag>();
-                fence_proxy_async_smem();
-                mbar_arrive(&sm.full[(it - kCorrLag) % kCorrStages]);
-            }
+            // Never block on the copies: the barrier phase completes when every
+            // producer's copies for this stage have landed. (A wait_group +
+            // proxy fence here drains ALL in-flight copies and serialises the
+            // ring to one stage — measured 18% of HBM bandwidth.)
+            cp_async_mbar_arrive(&sm.full[s]);
         }
         cp_async_wait<0>();
-        fence_proxy_async_smem();
-        for (int it = kchunks - kCorrLag > 0 ? kchunks - kCorrLag : 0; it < kchunks; ++it)
-            mbar_arrive(&sm.full[it % kCorrStages]);
 
         // ------------------------------------------------------ epilogue --
         mbar_wait(&sm.accum_full, 0);
@@ -220,6 +215,9 @@ __global__ void __launch_bounds__(kCorrThreads, 1) corr_detect_kernel(const __gr
             for (int it = 0; it < kchunks; ++it) {
                 const int s = it % kCorrStages;
                 mbar_wait(&sm.full[s], (it / kCorrStages) & 1);
+                // The stage's bytes are in smem (written through the generic
+                // proxy by cp.async); order them before the async-proxy MMA reads.
+                fence_proxy_async_smem();
                 tc_fence_after();
                 const uint32_t a_s = ring_u32 + s * kCorrStageBytes;
                 const uint64_t da = sw128_kmajor_desc(a_s);
@@ -326,55 +324,67 @@ __global__ void __launch_bounds__(256) detect_finish_kernel(const __grid_constan
             qrm_record rec;
             make_record(rec, raw, nerr, cw, nb, p.kbits, p.key_cw, p.key_msg, p.tau_msg, p.tau_raw,
                         __popcll(pe.tie_mask));
-            p.out[pe.image] = rec;
+            store_record(p.out + pe.image, rec);
         }
     }
+}
+
+// One output sample of the preprocess geometry: pixel (ox, oy) of the
+// (virtual) resized image, channel c — a direct read, or resize_bilinear
+// (image.cpp:57-85) evaluated in double with no FMA contraction.
+__device__ __forceinline__ uint8_t sample_pixel(const GatherDesc& d, int ox, int oy, int c) {
+    if (!d.upscale) return d.img[(static_cast<int64_t>(oy) * d.w + ox) * 3 + c];
+    const double sx = __ddiv_rn(static_cast<double>(d.w), static_cast<double>(d.sw));
+    const double sy = __ddiv_rn(static_cast<double>(d.h), static_cast<double>(d.sh));
+    const double fy = __dsub_rn(__dmul_rn(__dadd_rn(static_cast<double>(oy), 0.5), sy), 0.5);
+    const double y0d = floor(fy);
+    const double wy = __dsub_rn(fy, y0d);
+    const int y0 = min(max(static_cast<int>(y0d), 0), d.h - 1);
+    const int y1 = min(max(static_cast<int>(y0d) + 1, 0), d.h - 1);
+    const double fx = __dsub_rn(__dmul_rn(__dadd_rn(static_cast<double>(ox), 0.5), sx), 0.5);
+    const double x0d = floor(fx);
+    const double wx = __dsub_rn(fx, x0d);
+    const int x0 = min(max(static_cast<int>(x0d), 0), d.w - 1);
+    const int x1 = min(max(static_cast<int>(x0d) + 1, 0), d.w - 1);
+    auto at = [&](int x, int y) { return static_cast<double>(d.img[(static_cast<int64_t>(y) * d.w + x) * 3 + c]); };
+    const double omx = __dsub_rn(1.0, wx), omy = __dsub_rn(1.0, wy);
+    const double top = __dadd_rn(__dmul_rn(at(x0, y0), omx), __dmul_rn(at(x1, y0), wx));
+    const double bot = __dadd_rn(__dmul_rn(at(x0, y1), omx), __dmul_rn(at(x1, y1), wx));
+    double q = floor(__dadd_rn(__dadd_rn(__dmul_rn(top, omy), __dmul_rn(bot, wy)), 0.5));
+    q = fmin(fmax(q, 0.0), 255.0);
+    return static_cast<uint8_t>(q);
 }
 
 // Stages one l x l window per image into a contiguous [count][3 l^2] buffer:
 // the path for ragged batches, unaligned windows and inputs below the working
 // size, whose preprocess is a bilinear upscale (image.cpp:57-85 composed with
 // the centre crop, transforms.cpp:49-84) evaluated only on the window.
-
-
 __global__ void gather_windows_kernel(const GatherDesc* __restrict__ descs, int64_t count, int l,
                                       uint8_t* __restrict__ out) {
     const int K = 3 * l * l;
     for (int64_t img = blockIdx.y; img < count; img += gridDim.y) {
-    const GatherDesc d = descs[img];
-    uint8_t* dst = out + img * static_cast<int64_t>(K);
-    for (int px = blockIdx.x * blockDim.x + threadIdx.x; px < K; px += gridDim.x * blockDim.x) {
-        const int c = px % 3;
-        const int xy = px / 3;
-        const int ox = d.tx + xy % l + d.x_off;  // column in the (virtual) resized image
-        const int oy = d.ty + xy / l + d.y_off;
-        uint8_t v;
-        if (!d.upscale) {
-            v = d.img[(static_cast<int64_t>(oy) * d.w + ox) * 3 + c];
-        } else {
-            // resize_bilinear (image.cpp:57-85) in double, no FMA contraction.
-            const double sx = __ddiv_rn(static_cast<double>(d.w), static_cast<double>(d.sw));
-            const double sy = __ddiv_rn(static_cast<double>(d.h), static_cast<double>(d.sh));
-            const double fy = __dsub_rn(__dmul_rn(__dadd_rn(static_cast<double>(oy), 0.5), sy), 0.5);
-            const double y0d = floor(fy);
-            const double wy = __dsub_rn(fy, y0d);
-            const int y0 = min(max(static_cast<int>(y0d), 0), d.h - 1);
-            const int y1 = min(max(static_cast<int>(y0d) + 1, 0), d.h - 1);
-            const double fx = __dsub_rn(__dmul_rn(__dadd_rn(static_cast<double>(ox), 0.5), sx), 0.5);
-            const double x0d = floor(fx);
-            const double wx = __dsub_rn(fx, x0d);
-            const int x0 = min(max(static_cast<int>(x0d), 0), d.w - 1);
-            const int x1 = min(max(static_cast<int>(x0d) + 1, 0), d.w - 1);
-            auto at = [&](int x, int y) { return static_cast<double>(d.img[(static_cast<int64_t>(y) * d.w + x) * 3 + c]); };
-            const double omx = __dsub_rn(1.0, wx), omy = __dsub_rn(1.0, wy);
-            const double top = __dadd_rn(__dmul_rn(at(x0, y0), omx), __dmul_rn(at(x1, y0), wx));
-            const double bot = __dadd_rn(__dmul_rn(at(x0, y1), omx), __dmul_rn(at(x1, y1), wx));
-            double q = floor(__dadd_rn(__dadd_rn(__dmul_rn(top, omy), __dmul_rn(bot, wy)), 0.5));
-            q = fmin(fmax(q, 0.0), 255.0);
-            v = static_cast<uint8_t>(q);
+        const GatherDesc d = descs[img];
+        uint8_t* dst = out + img * static_cast<int64_t>(K);
+        for (int px = blockIdx.x * blockDim.x + threadIdx.x; px < K; px += gridDim.x * blockDim.x) {
+            const int c = px % 3, xy = px / 3;
+            dst[px] = sample_pixel(d, d.tx + xy % l + d.x_off, d.ty + xy / l + d.y_off, c);
         }
-        dst[px] = v;
     }
+}
+
+// Rectangular out_w x out_h window of one image (resize / crop / preprocess
+// host utilities), optionally normalised to float(v/127.5 - 1) (image.cpp:36).
+__global__ void resample_kernel(const GatherDesc d, int out_w, int out_h, int normalize, void* __restrict__ out) {
+    const int64_t n = static_cast<int64_t>(out_w) * out_h * 3;
+    for (int64_t px = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; px < n;
+         px += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int c = static_cast<int>(px % 3);
+        const int64_t xy = px / 3;
+        const uint8_t v = sample_pixel(d, static_cast<int>(xy % out_w) + d.x_off, static_cast<int>(xy / out_w) + d.y_off, c);
+        if (normalize)
+            static_cast<float*>(out)[px] = __double2float_rn(__dsub_rn(__ddiv_rn(static_cast<double>(v), 127.5), 1.0));
+        else
+            static_cast<uint8_t*>(out)[px] = v;
     }
 }
 
@@ -425,6 +435,15 @@ cudaError_t launch_gather_windows(const GatherDesc* descs, int64_t count, int l,
     const int K = 3 * l * l;
     dim3 grid(static_cast<unsigned>((K + 255) / 256), static_cast<unsigned>(count < 65535 ? count : 65535));
     gather_windows_kernel<<<grid, 256, 0, st>>>(descs, count, l, out);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_resample(const GatherDesc& d, int out_w, int out_h, int normalize, void* out, cudaStream_t st) {
+    const int64_t n = static_cast<int64_t>(out_w) * out_h * 3;
+    int64_t blocks = (n + 255) / 256;
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    if (blocks < 1) blocks = 1;
+    resample_kernel<<<static_cast<unsigned>(blocks), 256, 0, st>>>(d, out_w, out_h, normalize, out);
     return cudaGetLastError();
 }
 

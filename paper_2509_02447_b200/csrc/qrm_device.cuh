@@ -109,6 +109,11 @@ template <int N>
 QRM_D void cp_async_wait() {
     asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
+// Arrive on `bar` once all cp.async previously issued by this thread have
+// landed in shared memory (the barrier's count must include this thread).
+QRM_D void cp_async_mbar_arrive(uint64_t* bar) {
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
 // Make generic-proxy shared-memory writes visible to the async proxy (tcgen05.mma).
 QRM_D void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 

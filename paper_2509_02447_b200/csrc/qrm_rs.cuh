@@ -119,6 +119,18 @@ __device__ __forceinline__ void make_record(qrm_record& rec, uint64_t raw, int n
     }
 }
 
+// 24-byte record as three 8-byte stores (the struct's byte fields would
+// otherwise be written one ST.U8 at a time).
+__device__ __forceinline__ void store_record(qrm_record* dst, const qrm_record& r) {
+    const uint64_t info = static_cast<uint64_t>(r.status) | (static_cast<uint64_t>(r.errors) << 8) |
+                          (static_cast<uint64_t>(r.matches) << 16) | (static_cast<uint64_t>(r.verified) << 24) |
+                          (static_cast<uint64_t>(r.ties) << 32);
+    uint64_t* o = reinterpret_cast<uint64_t*>(dst);
+    o[0] = r.raw;
+    o[1] = r.msg;
+    o[2] = info;
+}
+
 // Partial syndromes of this lane's positions, reduced across the warp:
 // S_j = xor_i r_i v_i X_i^j for j < n-k (all lanes receive all S_j).
 template <int RMAX, int P>
