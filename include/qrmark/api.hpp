@@ -27,6 +27,7 @@
 #include <utility>
 #include <vector>
 
+#pragma GCC visibility push(default)
 namespace qrmark {
 
 // ------------------------------------------------------------- errors.hpp
@@ -134,6 +135,11 @@ private:
     std::vector<uint16_t> c_;
 };
 
+FieldElement operator+(FieldElement a, FieldElement b);
+FieldElement operator*(FieldElement a, FieldElement b);
+FieldElement operator/(FieldElement a, FieldElement b);
+Poly operator+(const Poly& a, const Poly& b);
+Poly operator*(const Poly& a, const Poly& b);
 Poly lagrange_interpolate(const FieldSpec& spec, std::span<const std::pair<uint16_t, uint16_t>> points);
 
 // ----------------------------------------------------------------- rs.hpp
@@ -426,3 +432,4 @@ std::pair<std::vector<DetectionRecord>, DeskReport> run_desk(const StreamPlan& p
                                                              const SyntheticStageLoad* load = nullptr);
 
 }  // namespace qrmark
+#pragma GCC visibility pop

@@ -1,0 +1,3 @@
+// Drop-in name for the reference header qrmark/errors.hpp; the declarations live in api.hpp.
+#pragma once
+#include "qrmark/api.hpp"

@@ -152,6 +152,20 @@ QRM_EXPORT qrm_status qrm_extract_device(qrm_ctx* ctx, const uint8_t* images, in
 /* preprocess (transforms.cpp:42-47) of one host image -> 256*256*3 floats. */
 QRM_EXPORT qrm_status qrm_preprocess_host(const uint8_t* image, int w, int h, float* out);
 
+/* General window resample of one host byte image on the device: pixel
+ * (x + x_off, y + y_off) of the image bilinearly resized to sw x sh
+ * (resize_bilinear, image.cpp:57-85; upscale = 0: the image itself), for an
+ * out_w x out_h window; u8 out, or float(v/127.5 - 1) (normalize,
+ * image.cpp:32-38) when normalize != 0. Covers resize_bilinear, center_crop
+ * (image.cpp:87-105), extract_tile (tiling.cpp:62-77) and preprocess. */
+QRM_EXPORT qrm_status qrm_resample_host(const uint8_t* image, int w, int h, int upscale, int sw, int sh, int x_off,
+                                        int y_off, int out_w, int out_h, int normalize, void* out);
+
+/* SpreadSpectrumCodec::extract (stego.cpp:53-67) of one normalised float tile
+ * (3 l^2 floats, any values): the reference's sequential double summation
+ * replayed on the device -> bit-identical soft values. */
+QRM_EXPORT qrm_status qrm_extract_float_host(uint64_t key_seed, int n_bits, int l, const float* tile, double* soft);
+
 /* ----------------------------------------------------------------- RS
  * Replace bw_decode (rs.cpp:188-196), bit-exact: the unique codeword within
  * distance t or failure. nerr_out[i] = errors_corrected, or -1 for a decode

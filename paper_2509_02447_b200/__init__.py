@@ -31,7 +31,7 @@ ABI_SYMBOLS = (
     "qrm_rs_decode_packed_device", "qrm_rs_decode_symbols_device", "qrm_rs_stress_device", "qrm_rs_encode_packed",
     "qrm_verify_threshold", "qrm_make_corpus_device", "qrm_patterns_device", "qrm_allocate_streams",
     "qrm_lpt_schedule", "qrm_warmup_profile", "qrm_ctx_set_plan", "qrm_kernel_launch_count",
-    "qrm_probe_decode_kernel",
+    "qrm_probe_decode_kernel", "qrm_resample_host", "qrm_extract_float_host",
 )
 
 

@@ -44,6 +44,8 @@ cudaError_t launch_rs_stress(const RsTables* tab, const uint64_t* enc_mask, uint
 cudaError_t launch_build_patterns(uint64_t seed, int nbits, int K, int K_pad, int8_t* pat, int32_t* colsum,
                                   cudaStream_t st);
 cudaError_t launch_residual(uint64_t seed, int nbits, int K, uint64_t codeword, float* delta, cudaStream_t st);
+cudaError_t launch_extract_float(uint64_t seed, int nbits, int K, const float* tile, double* soft, cudaStream_t st);
+cudaError_t launch_resample(const GatherDesc& d, int out_w, int out_h, int normalize, void* out, cudaStream_t st);
 cudaError_t launch_corpus(uint64_t first_seed, int64_t count, int w, int h, int l, int embed, float alpha,
                           const float* delta, uint8_t* out, cudaStream_t st);
 }  // namespace qrm
@@ -198,6 +200,7 @@ DetectParams base_params(qrm_ctx* c, Workspace& w, int64_t count, qrm_record* ou
     p.tau_msg = c->tau_msg;
     p.tau_raw = c->tau_raw;
     p.fuse_t1 = (c->t == 1 && c->n - c->k <= 3) ? 1 : 0;
+    if (const char* e = getenv("QRM_EXP_FLAGS")) p.exp_flags = atoi(e);
     p.key_cw = c->key_cw;
     p.key_msg = c->key_msg;
     p.patterns = c->d_patterns;
@@ -223,7 +226,33 @@ qrm_status run_detect(qrm_ctx* c, Workspace& w, const WindowSource& src, int64_t
     p.src = src;
     QRM_CUDA(cudaMemsetAsync(w.pending_count, 0, sizeof(int32_t), st));
     if (g_probe[0]) QRM_CUDA(cudaEventRecord(g_probe[0], st));
+    std::vector<unsigned long long> dbg;
+    unsigned long long* d_dbg = nullptr;
+    const int64_t max_ctas = ((count + 127) / 128) * 8;
+    if (getenv("QRM_DEBUG_TIMES")) {  // diagnostics: per-CTA phase timeline of the decode kernel
+        QRM_CUDA(cudaMalloc(&d_dbg, sizeof(unsigned long long) * 8 * max_ctas));
+        QRM_CUDA(cudaMemsetAsync(d_dbg, 0, sizeof(unsigned long long) * 8 * max_ctas, st));
+        p.dbg_times = d_dbg;
+    }
     QRM_LAUNCH(launch_corr_detect(p, c->sms, st));
+    if (d_dbg) {
+        dbg.resize(8 * max_ctas);
+        QRM_CUDA(cudaMemcpyAsync(dbg.data(), d_dbg, sizeof(unsigned long long) * dbg.size(), cudaMemcpyDeviceToHost, st));
+        QRM_CUDA(cudaStreamSynchronize(st));
+        cudaFree(d_dbg);
+        unsigned long long t0 = ~0ull;
+        for (int64_t i = 0; i < max_ctas; ++i)
+            if (dbg[i * 8]) t0 = std::min(t0, dbg[i * 8]);
+        for (int ph = 0; ph < 8; ++ph) {
+            std::vector<double> v;
+            for (int64_t i = 0; i < max_ctas; ++i)
+                if (dbg[i * 8 + ph]) v.push_back(static_cast<double>(dbg[i * 8 + ph] - t0) / 1e3);
+            std::sort(v.begin(), v.end());
+            if (!v.empty())
+                fprintf(stderr, "[qrm dbg] count=%lld phase %d: n=%zu min %.2f med %.2f max %.2f us\n",
+                        static_cast<long long>(count), ph, v.size(), v.front(), v[v.size() / 2], v.back());
+        }
+    }
     if (g_probe[1]) QRM_CUDA(cudaEventRecord(g_probe[1], st));
     cudaStream_t fs = st;
     if (mid_event && finish_stream) {
@@ -795,6 +824,47 @@ QRM_EXPORT qrm_status qrm_make_corpus_device(const qrm_config* cfg, uint64_t fir
         QRM_CUDA(cudaStreamSynchronize(as_stream(stream)));
         cudaFree(delta);
     }
+    return QRM_OK;
+}
+
+QRM_EXPORT qrm_status qrm_extract_float_host(uint64_t key_seed, int n_bits, int l, const float* tile, double* soft) {
+    if (!tile || !soft || n_bits <= 0 || l <= 0) return fail(QRM_INVALID_INPUT, "bad extract arguments");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return fail(QRM_NO_DEVICE, "no CUDA device available");
+    const int K = 3 * l * l;
+    float* dt = nullptr;
+    double* ds = nullptr;
+    QRM_CUDA(cudaMalloc(&dt, sizeof(float) * K));
+    QRM_CUDA(cudaMalloc(&ds, sizeof(double) * n_bits));
+    QRM_CUDA(cudaMemcpy(dt, tile, sizeof(float) * K, cudaMemcpyHostToDevice));
+    QRM_LAUNCH(launch_extract_float(key_seed, n_bits, K, dt, ds, nullptr));
+    QRM_CUDA(cudaMemcpy(soft, ds, sizeof(double) * n_bits, cudaMemcpyDeviceToHost));
+    cudaFree(dt);
+    cudaFree(ds);
+    return QRM_OK;
+}
+
+QRM_EXPORT qrm_status qrm_resample_host(const uint8_t* image, int w, int h, int upscale, int sw, int sh, int x_off,
+                                        int y_off, int out_w, int out_h, int normalize, void* out) {
+    if (!image || !out || w <= 0 || h <= 0 || out_w <= 0 || out_h <= 0)
+        return fail(QRM_INVALID_INPUT, "bad resample arguments");
+    if (!upscale && (x_off < 0 || y_off < 0 || x_off + out_w > w || y_off + out_h > h))
+        return fail(QRM_INVALID_INPUT, "window outside the image");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return fail(QRM_NO_DEVICE, "no CUDA device available");
+    const int64_t bytes = static_cast<int64_t>(w) * h * 3;
+    const int64_t n = static_cast<int64_t>(out_w) * out_h * 3;
+    const int64_t ob = n * (normalize ? sizeof(float) : 1);
+    uint8_t* dimg = nullptr;
+    void* dout = nullptr;
+    QRM_CUDA(cudaMalloc(&dimg, bytes));
+    QRM_CUDA(cudaMalloc(&dout, ob));
+    QRM_CUDA(cudaMemcpy(dimg, image, bytes, cudaMemcpyHostToDevice));
+    GatherDesc d{dimg, w, h, upscale, sw, sh, x_off, y_off, 0, 0};
+    QRM_LAUNCH(launch_resample(d, out_w, out_h, normalize, dout, nullptr));
+    QRM_CUDA(cudaMemcpy(out, dout, ob, cudaMemcpyDeviceToHost));
+    cudaFree(dimg);
+    cudaFree(dout);
     return QRM_OK;
 }
 

@@ -127,6 +127,28 @@ __global__ void __launch_bounds__(256) corpus_kernel(const __grid_constant__ Cor
     }
 }
 
+// SpreadSpectrumCodec::extract (stego.cpp:53-67) on an arbitrary normalised
+// float tile: one thread per bit replays the reference's sequential double
+// summation in pixel order (patterns regenerated from the counter RNG), so the
+// soft values are bit-identical to the reference's.
+__global__ void extract_float_kernel(uint64_t seed, int nbits, int K, const float* __restrict__ tile,
+                                     double* __restrict__ soft) {
+    const int bit = blockIdx.x * blockDim.x + threadIdx.x;
+    if (bit >= nbits) return;
+    double acc = 0.0;
+    for (int px = 0; px < K; ++px) {
+        const double d = static_cast<double>(tile[px]);
+        acc = (rng_word(seed, static_cast<uint64_t>(bit), static_cast<uint64_t>(px)) & 1) ? __dadd_rn(acc, d)
+                                                                                         : __dsub_rn(acc, d);
+    }
+    soft[bit] = __dmul_rn(acc, 1.0 / static_cast<double>(K));
+}
+
+cudaError_t launch_extract_float(uint64_t seed, int nbits, int K, const float* tile, double* soft, cudaStream_t st) {
+    extract_float_kernel<<<(nbits + 63) / 64, 64, 0, st>>>(seed, nbits, K, tile, soft);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_build_patterns(uint64_t seed, int nbits, int K, int K_pad, int8_t* pat, int32_t* colsum,
                                   cudaStream_t st) {
     cudaError_t e = cudaMemsetAsync(colsum, 0, sizeof(int32_t) * kMaxNBits, st);

@@ -93,6 +93,15 @@ __device__ __forceinline__ void finish_image(const DetectParams& p, const CorrSm
     store_record(p.out + img, rec);
 }
 
+// Diagnostics: per-CTA phase timestamps (thread 0), only when requested.
+__device__ __forceinline__ void dbg_mark(const DetectParams& p, int phase, int tid) {
+    if (p.dbg_times && tid == 0) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        p.dbg_times[static_cast<int64_t>(blockIdx.x) * 8 + phase] = t;
+    }
+}
+
 __device__ __forceinline__ const uint8_t* window_base(const WindowSource& s, int64_t img, int K) {
     if (!s.direct) return s.base + img * static_cast<int64_t>(K);
     int tx, ty;
@@ -114,6 +123,7 @@ __global__ void __launch_bounds__(kCorrThreads, 1) corr_detect_kernel(const __gr
     const int tid = threadIdx.x;
     const int warp = tid >> 5;
     const int lane = tid & 31;
+    dbg_mark(p, 0, tid);
     const uint32_t S = cluster_nctarank();  // 1 without a cluster launch
     const uint32_t rank = cluster_ctarank();
     const int64_t m0 = static_cast<int64_t>(blockIdx.x / S) * kCorrM;
@@ -137,6 +147,7 @@ __global__ void __launch_bounds__(kCorrThreads, 1) corr_detect_kernel(const __gr
     tc_fence_after();
     const uint32_t tmem = sm.tmem_base;
     const int rows_per = kCorrM / static_cast<int>(S);
+    dbg_mark(p, 1, tid);
 
     if (warp < 4) {
         // ------------------------------------------------------ producer --
@@ -180,7 +191,9 @@ __global__ void __launch_bounds__(kCorrThreads, 1) corr_detect_kernel(const __gr
         cp_async_wait<0>();
 
         // ------------------------------------------------------ epilogue --
+        dbg_mark(p, 2, tid);
         mbar_wait(&sm.accum_full, 0);
+        dbg_mark(p, 3, tid);
         tc_fence_after();
         uint32_t acc[kCorrN];
 #pragma unroll
@@ -192,11 +205,13 @@ __global__ void __launch_bounds__(kCorrThreads, 1) corr_detect_kernel(const __gr
         }
         tmem_ld_wait();
         tc_fence_before();
+        dbg_mark(p, 4, tid);
 
         const int row = warp * 32 + lane;
         if (S == 1) {
             const int64_t img = m0 + row;
             if (img < p.count) finish_image(p, sm, img, acc);
+            dbg_mark(p, 5, tid);
         } else {
             // push this partial row to its owner CTA: slot `rank`, local row
             const uint32_t owner = static_cast<uint32_t>(row / rows_per);
@@ -206,6 +221,7 @@ __global__ void __launch_bounds__(kCorrThreads, 1) corr_detect_kernel(const __gr
 #pragma unroll
             for (int q = 0; q < kCorrN / 4; ++q)
                 st_cluster_v4(dst + 16 * q, acc[4 * q], acc[4 * q + 1], acc[4 * q + 2], acc[4 * q + 3]);
+            dbg_mark(p, 5, tid);
         }
     } else if (warp == 4) {
         // ------------------------------------------------------ MMA issuer --
@@ -217,7 +233,7 @@ __global__ void __launch_bounds__(kCorrThreads, 1) corr_detect_kernel(const __gr
                 mbar_wait(&sm.full[s], (it / kCorrStages) & 1);
                 // The stage's bytes are in smem (written through the generic
                 // proxy by cp.async); order them before the async-proxy MMA reads.
-                fence_proxy_async_smem();
+                if (!(p.exp_flags & 1)) fence_proxy_async_smem();
                 tc_fence_after();
                 const uint32_t a_s = ring_u32 + s * kCorrStageBytes;
                 const uint64_t da = sw128_kmajor_desc(a_s);
@@ -233,6 +249,7 @@ __global__ void __launch_bounds__(kCorrThreads, 1) corr_detect_kernel(const __gr
     }
     if (S > 1) {
         cluster_sync_all();  // every partial row has landed in its owner's smem
+        dbg_mark(p, 6, tid);
         if (tid < rows_per) {
             uint32_t acc[kCorrN];
 #pragma unroll
@@ -252,6 +269,7 @@ __global__ void __launch_bounds__(kCorrThreads, 1) corr_detect_kernel(const __gr
             if (img < p.count) finish_image(p, sm, img, acc);
         }
     }
+    dbg_mark(p, 7, tid);
     __syncthreads();
     if (warp == 4) {
         tc_fence_after();
@@ -406,6 +424,10 @@ cudaError_t launch_corr_detect(const DetectParams& p, int sm_count, cudaStream_t
     const int sms = sm_count > 0 ? sm_count : 148;
     unsigned S = 1;
     while (S < 4 && tiles * S * 2 <= sms && (p.K_pad / kCorrKC) >= static_cast<int>(8 * S * 2)) S *= 2;
+    if (const char* env = getenv("QRM_CORR_KSPLIT")) {  // experiment hook
+        const int v = atoi(env);
+        if (v == 1 || v == 2 || v == 4 || v == 8) S = static_cast<unsigned>(v);
+    }
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(static_cast<unsigned>(tiles) * S);
     cfg.blockDim = dim3(kCorrThreads);

@@ -65,6 +65,8 @@ struct DetectParams {
     int32_t kbits;      // k*m
     int32_t tau_msg, tau_raw;
     int32_t fuse_t1;    // epilogue may run the t=1 RS decoder itself
+    int32_t exp_flags;  // experiment hooks (bit 0: skip the consumer proxy fence)
+    unsigned long long* dbg_times;  // nullable: per-CTA phase timestamps (globaltimer ns), 8 per CTA
     uint64_t key_cw, key_msg;
     const int8_t* patterns;   // [64][K_pad] s8, rows >= nbits zero
     const int32_t* colsum;    // [64] sum_px P_i[px]
