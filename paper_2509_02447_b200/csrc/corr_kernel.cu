@@ -1,0 +1,335 @@
+// Tile decode for the spread-spectrum watermark, sm_100a.
+//
+// Reference path (per image): preprocess (transforms.cpp:42-47) -> select_tile
+// (tiling.cpp:23-47) -> extract_tile (tiling.cpp:62-77) ->
+// SpreadSpectrumCodec::extract (stego.cpp:53-67) -> harden (stego.cpp:10-14)
+// -> bw_decode (rs.cpp:188) -> verify (detect.cpp:180-195).
+//
+// B200 restatement. The correlation is a GEMM D[img][bit] = sum_px A[img][px]
+// * P[bit][px] with A = the raw u8 tile window and P = the +-1 planes as s8.
+// Since normalize is v/127.5 - 1 and P is +-1, the reference's sign test on
+// sum_px float(v/127.5-1) P is the sign of the EXACT integer
+//   S = sum_px (2v - 255) P = 2 D - 255 colsum(P)
+// except when S == 0, where the reference's double rounding decides; those
+// (image, bit) pairs are re-evaluated with the reference's exact sequential
+// double summation by detect_finish_kernel, so hard bits are bit-exact.
+//
+// corr_detect_kernel: one CTA = 128 images (UMMA M) x 64 bit columns (N) x a
+// K range. Warps 0-3 stream 128-byte K chunks of the 128 tile windows
+// (cp.async, 16 B per thread, straight into the 128B-swizzled K-major operand
+// layout) and of the pattern matrix into a 6-stage smem ring, and prefetch the
+// tile rows 10 stages ahead into L2 (cp.async.bulk.prefetch) so the ring
+// refills at L2 rather than DRAM latency. Warp 4 issues tcgen05.mma kind::i8
+// (u8 x s8 -> s32, accumulators in TMEM). With few images the K range is split
+// over a cluster of 2 or 4 CTAs that reduce through DSMEM. The epilogue (one
+// image per thread = one TMEM lane) reads 64 columns with tcgen05.ld, forms S,
+// hardens, packs the raw word and — t = 1 codes without ties — runs the RS
+// decoder and verify in registers, so one launch produces final records.
+#include <cuda_runtime.h>
+
+#include <cstdlib>
+
+#include "qrm_device.cuh"
+#include "qrm_rs.cuh"
+#include "qrm_types.h"
+#include "qrm_window.cuh"
+
+namespace qrm {
+
+constexpr int kCorrM = 128;
+constexpr int kCorrN = 64;
+constexpr int kCorrKC = 128;  // bytes of K per stage
+constexpr int kCorrStages = 6;
+constexpr int kCorrABytes = kCorrM * kCorrKC;  // 16 KiB
+constexpr int kCorrBBytes = kCorrN * kCorrKC;  // 8 KiB
+constexpr int kCorrStageBytes = kCorrABytes + kCorrBBytes;
+constexpr int kCorrProducers = 128;
+constexpr int kCorrThreads = 160;
+constexpr int kPrefetchAhead = 10;     // stages of tile rows prefetched into L2 beyond the ring
+constexpr int kRedStride = kCorrN + 4;  // int32 words per reduction row (padded: conflict-free v4 access)
+
+struct CorrSmem {
+    uint64_t full[kCorrStages];
+    uint64_t empty[kCorrStages];
+    uint64_t accum_full;
+    uint32_t tmem_base;
+    alignas(16) int32_t thr[kCorrN];  // 255 * colsum(P_i): bit i = 2 D_i > thr_i
+    RsSmem rs;
+    // Split-K partials from the cluster: [rank][row within my 128/S rows][kRedStride]
+    alignas(16) int32_t red[kCorrM * kRedStride];
+};
+
+constexpr size_t kCorrSmemBytes = 1024 /*align slack*/ + kCorrStages * kCorrStageBytes + sizeof(CorrSmem);
+
+// Epilogue for one image (one TMEM lane): S_i = 2 D_i - 255 colsum_i; bit i =
+// S_i > 0 (harden), tie i = S_i == 0; pack MSB-first; t = 1 code without ties:
+// RS-correct + verify in registers. Straight-line: bits are gathered with
+// constant shifts and reversed once (the packed word is MSB-first).
+__device__ __forceinline__ void finish_image(const DetectParams& p, const CorrSmem& sm, int64_t img,
+                                             const uint32_t (&acc)[kCorrN]) {
+    const int nb = p.nbits;
+    uint32_t pos[2] = {0u, 0u}, zer[2] = {0u, 0u};
+    const int4* thr4 = reinterpret_cast<const int4*>(sm.thr);
+#pragma unroll
+    for (int q = 0; q < kCorrN / 4; ++q) {
+        const int4 t = thr4[q];
+        const int tv[4] = {t.x, t.y, t.z, t.w};
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int i = 4 * q + u;
+            const int s2 = 2 * static_cast<int>(acc[i]) - tv[u];
+            pos[i >> 5] |= static_cast<uint32_t>(s2 > 0) << (i & 31);
+            zer[i >> 5] |= static_cast<uint32_t>(s2 == 0) << (i & 31);
+        }
+    }
+    const uint64_t nmask = nb >= 64 ? ~0ull : ((1ull << nb) - 1);
+    const uint64_t tmask = ((static_cast<uint64_t>(zer[1]) << 32) | zer[0]) & nmask;
+    const uint64_t raw = __brevll((static_cast<uint64_t>(pos[1]) << 32) | pos[0]) >> (64 - nb);
+    if (p.soft) {
+        const double inv = 1.0 / (255.0 * static_cast<double>(p.K));
+#pragma unroll
+        for (int i = 0; i < kCorrN; ++i)  // constant indices keep acc[] in registers
+            if (i < nb) p.soft[img * nb + i] = static_cast<double>(2 * static_cast<int>(acc[i]) - sm.thr[i]) * inv;
+    }
+    if (p.raw_out) p.raw_out[img] = raw;
+    qrm_record rec;
+    if (tmask == 0 && p.fuse_t1) {
+        uint64_t cw = 0;
+        const int nerr = rs_t1_packed(sm.rs, raw, cw);
+        make_record(rec, raw, nerr, cw, nb, p.kbits, p.key_cw, p.key_msg, p.tau_msg, p.tau_raw, 0);
+    } else {
+        rec.raw = raw;
+        rec.msg = 0;
+        rec.status = kRecPending;
+        rec.errors = 0;
+        rec.matches = 0;
+        rec.verified = 0;
+        rec.ties = static_cast<uint8_t>(__popcll(tmask));
+        const int slot = atomicAdd(p.pending_count, 1);
+        p.pending[slot] = PendingEntry{img, tmask};
+    }
+    store_record(p.out + img, rec);
+}
+
+// Launched as clusters of S = 1, 2 or 4 CTAs along K (split-K): CTA r of a
+// cluster accumulates K chunks [r K/S, (r+1) K/S) of the same 128 images in its
+// own TMEM, pushes the partial rows owned by each peer into the peer's shared
+// memory (DSMEM), and after one cluster barrier each CTA finishes 128/S images.
+__global__ void __launch_bounds__(kCorrThreads, 1) corr_detect_kernel(const __grid_constant__ DetectParams p) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* ring = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    CorrSmem& sm = *reinterpret_cast<CorrSmem*>(ring + kCorrStages * kCorrStageBytes);
+
+    const int tid = threadIdx.x;
+    const int warp = tid >> 5;
+    const int lane = tid & 31;
+    dbg_mark(p, 0, tid);
+    const uint32_t S = cluster_nctarank();  // 1 without a cluster launch
+    const uint32_t rank = cluster_ctarank();
+    const int64_t m0 = static_cast<int64_t>(blockIdx.x / S) * kCorrM;
+    const int kc_total = p.K_pad / kCorrKC;
+    const int kc_begin = static_cast<int>(static_cast<int64_t>(kc_total) * rank / S);
+    const int kchunks = static_cast<int>(static_cast<int64_t>(kc_total) * (rank + 1) / S) - kc_begin;
+
+    if (warp == 4) tmem_alloc<kCorrN>(&sm.tmem_base);
+    if (tid == 0) {
+        for (int s = 0; s < kCorrStages; ++s) {
+            mbar_init(&sm.full[s], kCorrProducers);
+            mbar_init(&sm.empty[s], 1);
+        }
+        mbar_init(&sm.accum_full, 1);
+        mbar_fence_init();
+    }
+    if (tid < kCorrN) sm.thr[tid] = 255 * __ldg(p.colsum + tid);
+    if (p.fuse_t1) rs_stage_tables(sm.rs, p.rs, tid, kCorrThreads);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = sm.tmem_base;
+    const int rows_per = kCorrM / static_cast<int>(S);
+    dbg_mark(p, 1, tid);
+
+    if (warp < 4) {
+        // ------------------------------------------------------ producer --
+        const int c = tid & 7;    // 16-byte chunk within the 128-byte K chunk
+        const int rb = tid >> 3;  // rows rb + 16 j
+        const uint8_t* wb[8];
+        bool valid[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const int64_t img = m0 + rb + 16 * j;
+            valid[j] = img < p.count;
+            wb[j] = valid[j] ? window_base(p.src, img, p.K) : nullptr;
+        }
+        const int row_bytes = 3 * p.src.l;
+        const int pitch = p.src.direct ? p.src.pitch : row_bytes;
+        const uint32_t ring_u32 = smem_u32(ring);
+        // K offset of this thread's 16 B, as (tile row, column) — stepped, no division per stage.
+        int kbyte = kc_begin * kCorrKC + c * 16;
+        int trow = kbyte / row_bytes;
+        int tcol = kbyte - trow * row_bytes;
+        // L2 prefetch: thread (rb, c) prefetches the tile rows of image rb + 16 c.
+        const int64_t pf_img = m0 + rb + 16 * c;
+        const bool pf_on = pf_img < p.count && (row_bytes & 15) == 0;
+        const uint8_t* pf_base = pf_on ? window_base(p.src, pf_img, p.K) : nullptr;
+        const int k_end = (kc_begin + kchunks) * kCorrKC < p.K ? (kc_begin + kchunks) * kCorrKC : p.K;
+        int pf_row = (kc_begin * kCorrKC) / row_bytes;
+        for (int it = 0; it < kchunks; ++it) {
+            if (pf_on) {
+                int target = (kc_begin + it + 1 + kPrefetchAhead) * kCorrKC;
+                if (target > k_end) target = k_end;
+                while (pf_row * row_bytes < target) {
+                    prefetch_l2_bulk(pf_base + static_cast<int64_t>(pf_row) * pitch, static_cast<uint32_t>(row_bytes));
+                    ++pf_row;
+                }
+            }
+            const int s = it % kCorrStages;
+            mbar_wait(&sm.empty[s], ((it / kCorrStages) & 1) ^ 1);
+            const uint32_t a_s = ring_u32 + s * kCorrStageBytes;
+            const uint32_t b_s = a_s + kCorrABytes;
+            if (kbyte < p.K) {
+                const int64_t off = static_cast<int64_t>(trow) * pitch + tcol;
+#pragma unroll
+                for (int j = 0; j < 8; ++j)
+                    if (valid[j]) cp_async16(a_s + sw128_offset(rb + 16 * j, c), wb[j] + off);
+            }
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int n = rb + 16 * j;
+                cp_async16(b_s + sw128_offset(n, c), p.patterns + static_cast<int64_t>(n) * p.K_pad + kbyte);
+            }
+            // Never block on the copies: the barrier phase completes when every
+            // producer's copies for this stage have landed.
+            cp_async_mbar_arrive(&sm.full[s]);
+            kbyte += kCorrKC;
+            tcol += kCorrKC;
+            while (tcol >= row_bytes) {
+                tcol -= row_bytes;
+                ++trow;
+            }
+        }
+        cp_async_wait<0>();
+
+        // ------------------------------------------------------ epilogue --
+        dbg_mark(p, 2, tid);
+        mbar_wait(&sm.accum_full, 0);
+        dbg_mark(p, 3, tid);
+        tc_fence_after();
+        uint32_t acc[kCorrN];
+#pragma unroll
+        for (int q = 0; q < kCorrN / 16; ++q) {
+            uint32_t r16[16];
+            tmem_ld16(tmem + (static_cast<uint32_t>(warp * 32) << 16) + q * 16, r16);
+#pragma unroll
+            for (int i = 0; i < 16; ++i) acc[q * 16 + i] = r16[i];
+        }
+        tmem_ld_wait();
+        tc_fence_before();
+        dbg_mark(p, 4, tid);
+
+        const int row = warp * 32 + lane;
+        if (S == 1) {
+            const int64_t img = m0 + row;
+            if (img < p.count) finish_image(p, sm, img, acc);
+            dbg_mark(p, 5, tid);
+        } else {
+            // push this partial row to its owner CTA: slot `rank`, local row
+            const uint32_t owner = static_cast<uint32_t>(row / rows_per);
+            const uint32_t local = static_cast<uint32_t>(row % rows_per);
+            const uint32_t dst = map_to_rank(smem_u32(&sm.red[(rank * rows_per + local) * kRedStride]), owner);
+#pragma unroll
+            for (int q = 0; q < kCorrN / 4; ++q)
+                st_cluster_v4(dst + 16 * q, acc[4 * q], acc[4 * q + 1], acc[4 * q + 2], acc[4 * q + 3]);
+            dbg_mark(p, 5, tid);
+        }
+    } else if (warp == 4) {
+        // ------------------------------------------------------ MMA issuer --
+        if (lane == 0) {
+            const uint32_t idesc = idesc_i8_u8s8(kCorrM, kCorrN);
+            const uint32_t ring_u32 = smem_u32(ring);
+            for (int it = 0; it < kchunks; ++it) {
+                const int s = it % kCorrStages;
+                mbar_wait(&sm.full[s], (it / kCorrStages) & 1);
+                // The stage's bytes are in smem (written through the generic
+                // proxy by cp.async); order them before the async-proxy MMA reads.
+                if (!(p.exp_flags & 1)) fence_proxy_async_smem();
+                tc_fence_after();
+                const uint32_t a_s = ring_u32 + s * kCorrStageBytes;
+                const uint64_t da = sw128_kmajor_desc(a_s);
+                const uint64_t db = sw128_kmajor_desc(a_s + kCorrABytes);
+#pragma unroll
+                for (int k = 0; k < kCorrKC / 32; ++k)  // K = 32 bytes per kind::i8 MMA
+                    umma_i8(tmem, da + 2 * k, db + 2 * k, idesc, (it | k) != 0);
+                umma_commit(&sm.empty[s]);
+            }
+            umma_commit(&sm.accum_full);
+        }
+        __syncwarp();
+    }
+    if (S > 1) {
+        cluster_sync_all();  // every partial row has landed in its owner's smem
+        dbg_mark(p, 6, tid);
+        if (tid < rows_per) {
+            uint32_t acc[kCorrN];
+#pragma unroll
+            for (int i = 0; i < kCorrN; ++i) acc[i] = 0;
+            for (uint32_t s = 0; s < S; ++s) {
+                const int4* src = reinterpret_cast<const int4*>(&sm.red[(s * rows_per + tid) * kRedStride]);
+#pragma unroll
+                for (int q = 0; q < kCorrN / 4; ++q) {
+                    const int4 v = src[q];
+                    acc[4 * q] += v.x;
+                    acc[4 * q + 1] += v.y;
+                    acc[4 * q + 2] += v.z;
+                    acc[4 * q + 3] += v.w;
+                }
+            }
+            const int64_t img = m0 + static_cast<int64_t>(rank) * rows_per + tid;
+            if (img < p.count) finish_image(p, sm, img, acc);
+        }
+    }
+    dbg_mark(p, 7, tid);
+    __syncthreads();
+    if (warp == 4) {
+        tc_fence_after();
+        tmem_dealloc<kCorrN>(tmem);
+    }
+}
+
+cudaError_t launch_corr_detect(const DetectParams& p, int sm_count, cudaStream_t st) {
+    static bool configured = false;
+    if (!configured) {
+        cudaError_t e = cudaFuncSetAttribute(corr_detect_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             static_cast<int>(kCorrSmemBytes));
+        if (e != cudaSuccess) return e;
+        configured = true;
+    }
+    const int64_t tiles = (p.count + kCorrM - 1) / kCorrM;
+    if (tiles == 0) return cudaSuccess;
+    // Split K over a cluster when there are too few 128-image tiles to give
+    // every SM a CTA (one CTA per SM: the 6-stage ring uses ~180 KB of smem).
+    const int sms = sm_count > 0 ? sm_count : 148;
+    unsigned S = 1;
+    while (S < 4 && tiles * S * 2 <= sms && (p.K_pad / kCorrKC) >= static_cast<int>(8 * S * 2)) S *= 2;
+    if (const char* env = getenv("QRM_CORR_KSPLIT")) {  // experiment hook
+        const int v = atoi(env);
+        if (v == 1 || v == 2 || v == 4 || v == 8) S = static_cast<unsigned>(v);
+    }
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(static_cast<unsigned>(tiles) * S);
+    cfg.blockDim = dim3(kCorrThreads);
+    cfg.dynamicSmemBytes = kCorrSmemBytes;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = S;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, corr_detect_kernel, p);
+}
+
+size_t corr_smem_bytes() { return kCorrSmemBytes; }
+
+}  // namespace qrm

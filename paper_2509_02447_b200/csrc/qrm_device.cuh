@@ -58,8 +58,10 @@ QRM_HD void select_tile(int w, int h, int l, int strategy, uint64_t seed, uint64
         x = static_cast<int>(rng_below(seed, 2 * draw, 0, static_cast<uint64_t>(w - l) + 1));
         y = static_cast<int>(rng_below(seed, 2 * draw + 1, 0, static_cast<uint64_t>(h - l) + 1));
     } else {
-        const uint64_t cols = static_cast<uint64_t>(w / l), rows = static_cast<uint64_t>(h / l);
-        const uint64_t cell = rng_below(seed, draw, 0, cols * rows);
+        // cols*rows < 2^31 here (w, h are int), so the cell index fits 32 bits:
+        // 32-bit div/mod instead of a 64-bit division subroutine.
+        const uint32_t cols = static_cast<uint32_t>(w / l), rows = static_cast<uint32_t>(h / l);
+        const uint32_t cell = static_cast<uint32_t>(rng_below(seed, draw, 0, static_cast<uint64_t>(cols) * rows));
         x = static_cast<int>(cell % cols) * l;
         y = static_cast<int>(cell / cols) * l;
     }
@@ -113,6 +115,10 @@ QRM_D void cp_async_wait() {
 // landed in shared memory (the barrier's count must include this thread).
 QRM_D void cp_async_mbar_arrive(uint64_t* bar) {
     asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+// Fire-and-forget L2 prefetch of `bytes` (multiple of 16, 16-B aligned).
+QRM_D void prefetch_l2_bulk(const void* src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
 }
 // Make generic-proxy shared-memory writes visible to the async proxy (tcgen05.mma).
 QRM_D void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }

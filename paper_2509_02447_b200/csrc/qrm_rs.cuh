@@ -22,30 +22,14 @@
 namespace qrm {
 
 // Shared-memory copy of the tables a decoder needs.
-struct RsSmem {
-    int32_t m, n, k, t, r, q1, nmask, pad;
-    uint8_t exp2[512];
-    uint8_t log[256];
-    uint8_t logv[256];
-    uint64_t synd_mask[64];
-};
+// Same layout as the global image, so staging is a flat 16-byte-vector copy.
+using RsSmem = RsTables;
+static_assert(sizeof(RsTables) % 16 == 0, "RsTables must be copyable as uint4");
 
 __device__ __forceinline__ void rs_stage_tables(RsSmem& s, const RsTables* g, int tid, int nthreads) {
-    if (tid == 0) {
-        s.m = g->m;
-        s.n = g->n;
-        s.k = g->k;
-        s.t = g->t;
-        s.r = g->r;
-        s.q1 = g->q1;
-        s.nmask = g->nmask;
-    }
-    for (int i = tid; i < 512; i += nthreads) s.exp2[i] = g->exp2[i];
-    for (int i = tid; i < 256; i += nthreads) {
-        s.log[i] = g->log[i];
-        s.logv[i] = g->logv[i];
-    }
-    for (int i = tid; i < 64; i += nthreads) s.synd_mask[i] = g->synd_mask[i];
+    const uint4* src = reinterpret_cast<const uint4*>(g);
+    uint4* dst = reinterpret_cast<uint4*>(&s);
+    for (int i = tid; i < static_cast<int>(sizeof(RsTables) / 16); i += nthreads) dst[i] = __ldg(src + i);
 }
 
 __device__ __forceinline__ uint32_t gf_mul(const RsSmem& T, uint32_t a, uint32_t b) {
@@ -66,7 +50,13 @@ __device__ __forceinline__ int rs_t1_packed(const RsSmem& T, uint64_t word, uint
     for (int j = 0; j < 3; ++j) {
         if (j < r) {
             uint32_t s = 0;
-            for (int e = 0; e < m; ++e) s |= static_cast<uint32_t>(__popcll(word & T.synd_mask[j * m + e]) & 1) << e;
+            if (m == 4) {
+#pragma unroll
+                for (int e = 0; e < 4; ++e) s |= static_cast<uint32_t>(__popcll(word & T.synd_mask[j * 4 + e]) & 1) << e;
+            } else {
+#pragma unroll
+                for (int e = 0; e < 8; ++e) s |= static_cast<uint32_t>(__popcll(word & T.synd_mask[j * 8 + e]) & 1) << e;
+            }
             S[j] = s;
             any |= s;
         }

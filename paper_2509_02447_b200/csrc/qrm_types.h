@@ -14,7 +14,7 @@ constexpr uint8_t kRecPending = 0xFF;
 // GF(2^m) tables + GRS parity structure of an (n, k) evaluation code with
 // X_i = alpha^i (rs.cpp:52-63). Lives in device global memory; kernels stage
 // it into shared memory.
-struct RsTables {
+struct alignas(16) RsTables {
     int32_t m, n, k, t, r, q1;  // r = n - k, q1 = 2^m - 1
     int32_t packed_ok;          // n*m <= 64
     int32_t nmask;              // r*m syndrome-bit masks (packed words)
