@@ -168,7 +168,12 @@ namespace {
 
 qrm_status workspace_reserve(Workspace& w, int64_t count) {
     qrm_status s;
-    if (!w.pending_count) QRM_CUDA(cudaMalloc(&w.pending_count, sizeof(int32_t)));
+    if (!w.pending_count) {
+        // [0] pending entries, [1] finish-kernel block ticket; re-armed to 0 by
+        // the finish kernel itself after every launch.
+        QRM_CUDA(cudaMalloc(&w.pending_count, 2 * sizeof(int32_t)));
+        QRM_CUDA(cudaMemset(w.pending_count, 0, 2 * sizeof(int32_t)));
+    }
     if ((s = ensure(w.pending, w.pending_cap, count)) != QRM_OK) return s;
     return QRM_OK;
 }
@@ -224,11 +229,10 @@ qrm_status run_detect(qrm_ctx* c, Workspace& w, const WindowSource& src, int64_t
     if (s != QRM_OK) return s;
     DetectParams p = base_params(c, w, count, out, soft, raw);
     p.src = src;
-    QRM_CUDA(cudaMemsetAsync(w.pending_count, 0, sizeof(int32_t), st));
     if (g_probe[0]) QRM_CUDA(cudaEventRecord(g_probe[0], st));
     std::vector<unsigned long long> dbg;
     unsigned long long* d_dbg = nullptr;
-    const int64_t max_ctas = ((count + 127) / 128) * 8;
+    const int64_t max_ctas = ((count + 15) / 16) * 4 + 8;
     if (getenv("QRM_DEBUG_TIMES")) {  // diagnostics: per-CTA phase timeline of the decode kernel
         QRM_CUDA(cudaMalloc(&d_dbg, sizeof(unsigned long long) * 8 * max_ctas));
         QRM_CUDA(cudaMemsetAsync(d_dbg, 0, sizeof(unsigned long long) * 8 * max_ctas, st));
@@ -394,6 +398,10 @@ QRM_EXPORT qrm_status qrm_ctx_create(int device, const qrm_config* cfg, qrm_ctx*
     c->K = 3 * c->l * c->l;
     c->K_pad = (c->K + 127) / 128 * 128;
     QRM_CUDA(cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, device));
+    if (const char* g = getenv("QRM_L2_FETCH")) {  // experiment hook: max L2 fetch granularity (bytes)
+        cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, static_cast<size_t>(atoi(g)));
+        cudaGetLastError();
+    }
     for (int i = 0; i < kbits; ++i) c->key_msg = (c->key_msg << 1) | (c->key_message[i] & 1);
     c->key_cw = encode_packed(c->m, c->n, c->k, c->key_msg);
     c->tau_msg = verify_threshold(kbits, cfg->fpr_target);

@@ -36,11 +36,14 @@ __device__ __forceinline__ bool reference_tie_bit(const WindowSource& s, int64_t
 template <int TMAX>
 __global__ void __launch_bounds__(256) detect_finish_kernel(const __grid_constant__ DetectParams p) {
     __shared__ RsSmem T;
-    rs_stage_tables(T, p.rs, threadIdx.x, blockDim.x);
+    __shared__ int npend_s;
+    if (threadIdx.x == 0) npend_s = *reinterpret_cast<volatile int32_t*>(p.pending_count);
+    __syncthreads();
+    const int npend = npend_s;
+    if (npend > 0) rs_stage_tables(T, p.rs, threadIdx.x, blockDim.x);  // nothing to do: skip the staging
     __syncthreads();
     const int lane = threadIdx.x & 31;
     const int64_t warps = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
-    const int npend = *p.pending_count;
     for (int64_t e = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5); e < npend;
          e += warps) {
         const PendingEntry pe = p.pending[e];
@@ -79,6 +82,18 @@ __global__ void __launch_bounds__(256) detect_finish_kernel(const __grid_constan
             make_record(rec, raw, nerr, cw, nb, p.kbits, p.key_cw, p.key_msg, p.tau_msg, p.tau_raw,
                         __popcll(pe.tie_mask));
             store_record(p.out + pe.image, rec);
+        }
+    }
+    // The last block to finish re-arms the pending counter for the next
+    // launch (pending_count[1] is the block ticket), so no memset is needed.
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        const int ticket = atomicAdd(p.pending_count + 1, 1);
+        if (ticket == static_cast<int>(gridDim.x) - 1) {
+            p.pending_count[0] = 0;
+            p.pending_count[1] = 0;
+            __threadfence();
         }
     }
 }

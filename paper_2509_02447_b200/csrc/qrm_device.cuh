@@ -120,6 +120,8 @@ QRM_D void cp_async_mbar_arrive(uint64_t* bar) {
 QRM_D void prefetch_l2_bulk(const void* src, uint32_t bytes) {
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
 }
+// Prefetch the line holding `p` into L2 (plain LSU prefetch).
+QRM_D void prefetch_l2_line(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
 // Make generic-proxy shared-memory writes visible to the async proxy (tcgen05.mma).
 QRM_D void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
