@@ -321,10 +321,11 @@ def main():
                        "global_batch": BATCH * world, "per_gpu_batch": BATCH, "parallelism": f"dp{world} (shards)",
                        "l2": "inputs rotate over a 16,384-image pool (3.2 GB; each step a different batch and "
                              "draw range, 4 x 50 MB of tile windows per rotation > 126 MB L2)",
-                       "e2e_modes": {"staged_window (mode 2, headline)": e2e[2],
-                                     "mapped_window_zero_copy (mode 0)": e2e[0],
-                                     "full_image_h2d (mode 1)": e2e[1]}},
-            "e2e": e2e[2],
+                       "e2e_modes": {"mapped_window_zero_copy (mode 0, headline)": e2e[0],
+                                     "staged_window_host_gather (mode 2)": e2e[2],
+                                     "full_image_h2d (mode 1)": e2e[1]},
+                       "e2e_plan": {"streams": plan[0], "minibatch": plan[1]}},
+            "e2e": e2e[0],
             "gpu_launches": launches,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                          "frac": achieved / hbm, "traffic": traffic, "kernel": "corr_detect_kernel",

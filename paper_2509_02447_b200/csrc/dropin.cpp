@@ -773,7 +773,7 @@ std::vector<DetectionRecord> DetectionContext::detect_many(std::span<const Image
             }
         }
         const qrm_status s = qrm_detect_host(gpu_->h, pinned, n, w, h, static_cast<int64_t>(bytes), first_draw,
-                                             rec.data(), &pl, 2, nullptr);
+                                             rec.data(), &pl, 0, nullptr);  // mapped-window transfer
         cudaFreeHost(pinned);
         check(s);
     } else {
