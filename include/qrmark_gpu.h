@@ -149,6 +149,16 @@ QRM_EXPORT qrm_status qrm_extract_device(qrm_ctx* ctx, const uint8_t* images, in
                                          int64_t image_stride, uint64_t first_draw, double* soft, uint64_t* raw,
                                          void* stream);
 
+/* The learned extractor behind the WatermarkCodec plug-in point
+ * (stego.hpp:32-40): a HiDDeN / Stable-Signature-style conv stack (9 x conv3x3
+ * + BN + ReLU at 64x64, avg-pool, linear; contract in oracle/hidden_oracle.c)
+ * with random-init weights drawn from `weight_seed`, run as implicit-GEMM
+ * tcgen05 bf16 kernels, then the same RS correction and verify as
+ * qrm_detect_device. logits (count x n*m floats) is nullable. Needs l = 64. */
+QRM_EXPORT qrm_status qrm_hidden_detect_device(qrm_ctx* ctx, const uint8_t* images, int64_t count, int w, int h,
+                                               int64_t image_stride, uint64_t first_draw, uint64_t weight_seed,
+                                               float* logits, qrm_record* out, void* stream);
+
 /* preprocess (transforms.cpp:42-47) of one host image -> 256*256*3 floats. */
 QRM_EXPORT qrm_status qrm_preprocess_host(const uint8_t* image, int w, int h, float* out);
 

@@ -160,10 +160,52 @@ class Oracle(_Common):
         L.orc_allocate_streams.argtypes = [C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_double), C.c_double,
                                            C.c_int, C.c_int, C.c_double, C.c_double, C.c_int, C.POINTER(C.c_int),
                                            C.POINTER(C.c_int), C.POINTER(C.c_double)]
+        L.orc_hidden_weight.restype = C.c_float
+        L.orc_hidden_weight.argtypes = [C.c_uint64, C.c_int, C.c_int, C.c_int, C.c_int]
+        L.orc_hidden_bn.argtypes = [C.c_uint64, C.c_int, C.c_int] + [C.POINTER(C.c_float)] * 4
+        L.orc_hidden_linear_w.restype = C.c_float
+        L.orc_hidden_linear_w.argtypes = [C.c_uint64, C.c_int, C.c_int, C.c_int]
+        L.orc_hidden_linear_b.restype = C.c_float
+        L.orc_hidden_linear_b.argtypes = [C.c_uint64, C.c_int]
+        L.orc_hidden_forward.argtypes = [C.c_uint64, C.c_int, C.c_int, C.POINTER(C.c_uint8), C.POINTER(C.c_double),
+                                         C.POINTER(C.c_double)]
         L.orc_lpt_schedule.argtypes = ([C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_double), C.POINTER(C.c_double),
                                         C.POINTER(C.c_int), C.c_int, C.c_double, C.c_double, C.c_int, C.c_int,
                                         C.c_int] + [C.POINTER(C.c_int)] * 3 + [C.POINTER(C.c_double)] * 2 +
                                        [C.POINTER(C.c_int)] * 2 + [C.POINTER(C.c_double), C.POINTER(C.c_int)])
+
+    # -- learned extractor (hidden_oracle.c)
+    def hidden_forward(self, seed, nbits, tile_u8):
+        """fp32 conv-stack logits (double accumulation) of one l x l x 3 u8 tile."""
+        t = np.ascontiguousarray(tile_u8, np.uint8)
+        lg = np.zeros(nbits)
+        pooled = np.zeros(nbits)
+        self.lib.orc_hidden_forward(seed, nbits, t.shape[0], _u8p(t), _p(lg, C.c_double), _p(pooled, C.c_double))
+        return lg, pooled
+
+    def hidden_params(self, seed, nbits):
+        """All parameters as numpy arrays (for the torch cross-check)."""
+        L = self.lib
+        Ws, bns = [], []
+        for j in range(9):
+            cin = 3 if j == 0 else 64
+            cout = nbits if j == 8 else 64
+            w = np.zeros((cout, 9, cin), np.float32)
+            for co in range(cout):
+                for t in range(9):
+                    for ci in range(cin):
+                        w[co, t, ci] = L.orc_hidden_weight(seed, j, co, t, ci)
+            Ws.append(w)
+            g, b, m, v = (C.c_float() for _ in range(4))
+            bn = np.zeros((4, cout), np.float32)
+            for c in range(cout):
+                L.orc_hidden_bn(seed, j, c, C.byref(g), C.byref(b), C.byref(m), C.byref(v))
+                bn[:, c] = (g.value, b.value, m.value, v.value)
+            bns.append(bn)
+        wl = np.array([[L.orc_hidden_linear_w(seed, nbits, o, i) for i in range(nbits)] for o in range(nbits)],
+                      np.float32)
+        bl = np.array([L.orc_hidden_linear_b(seed, o) for o in range(nbits)], np.float32)
+        return Ws, bns, wl, bl
 
     # -- primitives
     def rng_word(self, s, st, c):

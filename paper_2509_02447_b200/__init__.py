@@ -31,7 +31,7 @@ ABI_SYMBOLS = (
     "qrm_rs_decode_packed_device", "qrm_rs_decode_symbols_device", "qrm_rs_stress_device", "qrm_rs_encode_packed",
     "qrm_verify_threshold", "qrm_make_corpus_device", "qrm_patterns_device", "qrm_allocate_streams",
     "qrm_lpt_schedule", "qrm_warmup_profile", "qrm_ctx_set_plan", "qrm_kernel_launch_count",
-    "qrm_probe_decode_kernel", "qrm_resample_host", "qrm_extract_float_host",
+    "qrm_probe_decode_kernel", "qrm_resample_host", "qrm_extract_float_host", "qrm_hidden_detect_device",
 )
 
 
@@ -115,6 +115,9 @@ def lib() -> C.CDLL:
         L.qrm_warmup_profile.argtypes = [vp, vp, i64, i32, i32, i64, i32, i32, vp, vp]
         L.qrm_ctx_set_plan.argtypes = [vp, C.POINTER(_Plan)]
         L.qrm_probe_decode_kernel.argtypes = [vp, vp, i64, i32, i32, i64, i32, C.POINTER(C.c_double)]
+        L.qrm_hidden_detect_device.argtypes = [vp, vp, i64, i32, i32, i64, u64, u64, vp, vp, vp]
+        L.qrm_resample_host.argtypes = [vp, i32, i32, i32, i32, i32, i32, i32, i32, i32, i32, vp]
+        L.qrm_extract_float_host.argtypes = [u64, i32, i32, vp, vp]
         _lib = L
     return _lib
 
@@ -412,6 +415,21 @@ class DetectionContext:
         _check(lib().qrm_detect_device(self._h, _ptr(images), B, W, H, images.stride(0), first_draw, _ptr(out),
                                        _stream(stream)))
         return out
+
+    def hidden_detect_device(self, images, weight_seed: int = 7, first_draw: int = 0, logits: bool = True,
+                             out=None, stream=None):
+        """Learned extractor (HiDDeN-style conv stack on tcgen05, bf16) + RS + verify on a device batch.
+
+        -> (logits float32 [B, N] or None, record tensor [B, 24] uint8)."""
+        import torch
+        B, H, W, _ = images.shape
+        nb = self.cfg.code.codeword_bits()
+        lg = torch.empty((B, nb), dtype=torch.float32, device=images.device) if logits else None
+        if out is None:
+            out = torch.empty((B, RECORD_DTYPE.itemsize), dtype=torch.uint8, device=images.device)
+        _check(lib().qrm_hidden_detect_device(self._h, _ptr(images), B, W, H, images.stride(0), first_draw,
+                                              weight_seed, _ptr(lg), _ptr(out), _stream(stream)))
+        return lg, out
 
     def extract_device(self, images, first_draw: int = 0, soft: bool = True, stream=None):
         """SpreadSpectrumCodec::extract + harden on a device batch -> (soft float64 [B, N] or None, raw int64 [B])."""

@@ -28,7 +28,10 @@
 #include "qrm_device.cuh"
 #include "qrm_types.h"
 #include "qrmark_gpu.h"
+#include <cudaTypedefs.h>
+
 #include "host_pool.hpp"
+#include "qrm_hidden.h"
 #include "sched_host.hpp"
 
 namespace qrm {
@@ -162,6 +165,16 @@ struct qrm_ctx {
     std::vector<cudaStream_t> streams;
     qrm_plan plan{{1, 2, 1}, {4096, 4096, 4096}};
     std::unique_ptr<HostPool> pool;  // window staging workers (host pipeline, mode 2)
+    // learned (conv) extractor: folded weights + activation ping-pong buffers
+    struct Hidden {
+        bool ready = false;
+        uint64_t seed = 0;
+        __nv_bfloat16* w_sw = nullptr;  // [8][9][64][64] swizzled, layers 1..8
+        float *bias = nullptr, *w0 = nullptr, *wl = nullptr, *bl = nullptr, *pool = nullptr;
+        __nv_bfloat16* act[2] = {nullptr, nullptr};
+        int64_t tiles_cap = 0;
+        CUtensorMap tmap[2];
+    } hid;
 };
 
 namespace {
@@ -281,13 +294,13 @@ bool direct_ok(const qrm_ctx* c, const uint8_t* base, int w, int h, int64_t stri
 
 // Uniform batch at `images` (device-accessible) -> records, choosing the direct
 // window path when alignment allows and the gather path otherwise.
-qrm_status detect_uniform(qrm_ctx* c, Workspace& w, const uint8_t* images, int64_t count, int width, int height,
-                          int64_t stride, uint64_t first_draw, qrm_record* out, double* soft, uint64_t* raw,
-                          cudaStream_t st, cudaEvent_t mid = nullptr, cudaStream_t fs = nullptr) {
-    if (count == 0) return QRM_OK;
+// Where the decode kernels read each image's l x l window: straight from the
+// images when alignment allows, else from windows staged by the gather kernel.
+qrm_status window_source(qrm_ctx* c, Workspace& w, const uint8_t* images, int64_t count, int width, int height,
+                         int64_t stride, uint64_t first_draw, cudaStream_t st, WindowSource& src) {
     int up, sw, sh, xo, yo;
     geometry(width, height, up, sw, sh, xo, yo);
-    WindowSource src{};
+    src = WindowSource{};
     src.l = c->l;
     src.strategy = c->cfg.tile_strategy;
     src.tile_seed = c->cfg.tile_seed;
@@ -299,25 +312,35 @@ qrm_status detect_uniform(qrm_ctx* c, Workspace& w, const uint8_t* images, int64
         src.x_off = xo;
         src.y_off = yo;
         src.direct = 1;
-    } else {
-        qrm_status s;
-        if ((s = ensure(w.stage, w.stage_cap, count * c->K)) != QRM_OK) return s;
-        if ((s = ensure(w.descs, w.desc_cap, count)) != QRM_OK) return s;
-        std::vector<GatherDesc> d(count);
-        for (int64_t i = 0; i < count; ++i) {
-            int tx, ty;
-            select_tile(kWorkingSize, kWorkingSize, c->l, c->cfg.tile_strategy, c->cfg.tile_seed,
-                        first_draw + static_cast<uint64_t>(i), tx, ty);
-            d[i] = GatherDesc{images + i * stride, width, height, up, sw, sh, xo, yo, tx, ty};
-        }
-        QRM_CUDA(cudaMemcpyAsync(w.descs, d.data(), sizeof(GatherDesc) * count, cudaMemcpyHostToDevice, st));
-        QRM_LAUNCH(launch_gather_windows(w.descs, count, c->l, w.stage, st));
-        QRM_CUDA(cudaStreamSynchronize(st));  // the pageable descriptor copy must finish before `d` dies
-        src.base = w.stage;
-        src.image_stride = c->K;
-        src.pitch = 3 * c->l;
-        src.direct = 0;
+        return QRM_OK;
     }
+    qrm_status s;
+    if ((s = ensure(w.stage, w.stage_cap, count * c->K)) != QRM_OK) return s;
+    if ((s = ensure(w.descs, w.desc_cap, count)) != QRM_OK) return s;
+    std::vector<GatherDesc> d(count);
+    for (int64_t i = 0; i < count; ++i) {
+        int tx, ty;
+        select_tile(kWorkingSize, kWorkingSize, c->l, c->cfg.tile_strategy, c->cfg.tile_seed,
+                    first_draw + static_cast<uint64_t>(i), tx, ty);
+        d[i] = GatherDesc{images + i * stride, width, height, up, sw, sh, xo, yo, tx, ty};
+    }
+    QRM_CUDA(cudaMemcpyAsync(w.descs, d.data(), sizeof(GatherDesc) * count, cudaMemcpyHostToDevice, st));
+    QRM_LAUNCH(launch_gather_windows(w.descs, count, c->l, w.stage, st));
+    QRM_CUDA(cudaStreamSynchronize(st));  // the pageable descriptor copy must finish before `d` dies
+    src.base = w.stage;
+    src.image_stride = c->K;
+    src.pitch = 3 * c->l;
+    src.direct = 0;
+    return QRM_OK;
+}
+
+qrm_status detect_uniform(qrm_ctx* c, Workspace& w, const uint8_t* images, int64_t count, int width, int height,
+                          int64_t stride, uint64_t first_draw, qrm_record* out, double* soft, uint64_t* raw,
+                          cudaStream_t st, cudaEvent_t mid = nullptr, cudaStream_t fs = nullptr) {
+    if (count == 0) return QRM_OK;
+    WindowSource src;
+    const qrm_status s = window_source(c, w, images, count, width, height, stride, first_draw, st, src);
+    if (s != QRM_OK) return s;
     return run_detect(c, w, src, count, out, soft, raw, st, mid, fs);
 }
 
@@ -424,6 +447,14 @@ QRM_EXPORT void qrm_ctx_destroy(qrm_ctx* c) {
     cudaFree(c->d_patterns);
     cudaFree(c->d_colsum);
     cudaFree(c->d_records);
+    cudaFree(c->hid.w_sw);
+    cudaFree(c->hid.bias);
+    cudaFree(c->hid.w0);
+    cudaFree(c->hid.wl);
+    cudaFree(c->hid.bl);
+    cudaFree(c->hid.pool);
+    cudaFree(c->hid.act[0]);
+    cudaFree(c->hid.act[1]);
     delete c;
 }
 
@@ -832,6 +863,117 @@ QRM_EXPORT qrm_status qrm_make_corpus_device(const qrm_config* cfg, uint64_t fir
         QRM_CUDA(cudaStreamSynchronize(as_stream(stream)));
         cudaFree(delta);
     }
+    return QRM_OK;
+}
+
+}  // extern "C"
+
+namespace {
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda).
+qrm_status encode_act_tmap(CUtensorMap* map, void* base, int64_t tiles) {
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+    if (!encode) {
+        cudaDriverEntryPointQueryResult q;
+        void* fn = nullptr;
+        QRM_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+        if (q != cudaDriverEntryPointSuccess || !fn) return fail(QRM_CUDA_ERROR, "cuTensorMapEncodeTiled unavailable");
+        encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    }
+    // activations NHWC bf16 [T][64 y][64 x][64 c]; box = 4 rows of 64 pixels
+    const cuuint64_t dims[4] = {64, 64, 64, static_cast<cuuint64_t>(tiles)};
+    const cuuint64_t strides[3] = {64 * 2, 64 * 64 * 2, 64 * 64 * 64 * 2};
+    const cuuint32_t box[4] = {64, 64, 4, 1};
+    const cuuint32_t estr[4] = {1, 1, 1, 1};
+    const CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, base, dims, strides, box, estr,
+                              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(QRM_CUDA_ERROR, "cuTensorMapEncodeTiled failed (" + std::to_string(r) + ")");
+    return QRM_OK;
+}
+
+qrm_status hidden_prepare(qrm_ctx* c, uint64_t seed, int64_t tiles, cudaStream_t st) {
+    auto& H = c->hid;
+    if (!H.w_sw) {
+        QRM_CUDA(cudaMalloc(&H.w_sw, sizeof(__nv_bfloat16) * 8 * 9 * 64 * 64));
+        QRM_CUDA(cudaMalloc(&H.bias, sizeof(float) * 9 * 64));
+        QRM_CUDA(cudaMalloc(&H.w0, sizeof(float) * 27 * 64));
+        QRM_CUDA(cudaMalloc(&H.wl, sizeof(float) * 64 * 64));
+        QRM_CUDA(cudaMalloc(&H.bl, sizeof(float) * 64));
+    }
+    if (!H.ready || H.seed != seed) {
+        QRM_LAUNCH(launch_hidden_prep(seed, c->nbits, H.w_sw, H.bias, H.w0, H.wl, H.bl, st));
+        H.ready = true;
+        H.seed = seed;
+    }
+    if (tiles > H.tiles_cap) {
+        for (auto& a : H.act) cudaFree(a);
+        cudaFree(H.pool);
+        const size_t act_bytes = sizeof(__nv_bfloat16) * 64 * 64 * 64 * static_cast<size_t>(tiles);
+        QRM_CUDA(cudaMalloc(&H.act[0], act_bytes));
+        QRM_CUDA(cudaMalloc(&H.act[1], act_bytes));
+        QRM_CUDA(cudaMalloc(&H.pool, sizeof(float) * kHiddenBlocksPerTile * 64 * tiles));
+        qrm_status s;
+        for (int i = 0; i < 2; ++i)
+            if ((s = encode_act_tmap(&H.tmap[i], H.act[i], tiles)) != QRM_OK) return s;
+        H.tiles_cap = tiles;
+    }
+    return QRM_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+QRM_EXPORT qrm_status qrm_hidden_detect_device(qrm_ctx* c, const uint8_t* images, int64_t count, int w, int h,
+                                               int64_t stride, uint64_t first_draw, uint64_t weight_seed,
+                                               float* logits, qrm_record* out, void* stream) {
+    qrm_status s = check_uniform(c, images, count, w, h, stride);
+    if (s != QRM_OK) return s;
+    if (count > 0 && !out) return fail(QRM_INVALID_INPUT, "null record buffer");
+    if (c->l != 64) return fail(QRM_INVALID_INPUT, "the conv extractor is defined on 64x64 tiles");
+    if ((s = set_device(c->device)) != QRM_OK) return s;
+    if (count == 0) return QRM_OK;
+    cudaStream_t st = as_stream(stream);
+    Workspace& W = c->ws[0];
+    if ((s = hidden_prepare(c, weight_seed, count, st)) != QRM_OK) return s;
+    if ((s = workspace_reserve(W, count)) != QRM_OK) return s;
+    WindowSource src;
+    if ((s = window_source(c, W, images, count, w, h, stride, first_draw, st, src)) != QRM_OK) return s;
+    auto& H = c->hid;
+    Conv0Params p0{src, count, c->K, H.w0, H.bias, H.act[0]};
+    QRM_LAUNCH(launch_conv0(p0, st));
+    for (int j = 1; j < kHiddenLayers; ++j) {
+        HiddenLayerParams lp{};
+        lp.w_swizzled = H.w_sw + static_cast<int64_t>(j - 1) * 9 * 64 * 64;
+        lp.bias = H.bias + j * 64;
+        lp.last = j == kHiddenLayers - 1;
+        lp.act_out = lp.last ? nullptr : H.act[j & 1];
+        lp.pool_out = lp.last ? H.pool : nullptr;
+        lp.tiles = count;
+        QRM_LAUNCH(launch_conv64(H.tmap[(j - 1) & 1], lp, c->sms, st));
+    }
+    HeadParams hp{};
+    hp.pool = H.pool;
+    hp.wl = H.wl;
+    hp.bl = H.bl;
+    hp.tiles = count;
+    hp.nbits = c->nbits;
+    hp.kbits = c->kbits;
+    hp.tau_msg = c->tau_msg;
+    hp.tau_raw = c->tau_raw;
+    hp.fuse_t1 = (c->t == 1 && c->n - c->k <= 3) ? 1 : 0;
+    hp.key_cw = c->key_cw;
+    hp.key_msg = c->key_msg;
+    hp.rs = c->d_rs;
+    hp.logits = logits;
+    hp.out = out;
+    hp.pending_count = W.pending_count;
+    hp.pending = W.pending;
+    QRM_LAUNCH(launch_hidden_head(hp, st));
+    DetectParams fp = base_params(c, W, count, out, nullptr, nullptr);
+    fp.src = src;
+    QRM_LAUNCH(launch_detect_finish(fp, std::max(1, c->t), c->sms, st));  // general-t codes only
     return QRM_OK;
 }
 

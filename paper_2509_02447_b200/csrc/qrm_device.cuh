@@ -162,6 +162,43 @@ QRM_D void umma_bf16(uint32_t tmem_d, uint64_t desc_a, uint64_t desc_b, uint32_t
         : "memory");
 }
 
+// As umma_bf16, with output lanes disabled (mask bit set = lane not written):
+// mask[q] covers lanes 32q..32q+31.
+QRM_D void umma_bf16_masked(uint32_t tmem_d, uint64_t desc_a, uint64_t desc_b, uint32_t idesc, uint32_t accumulate,
+                            uint32_t m0, uint32_t m1, uint32_t m2, uint32_t m3) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, {%5, %6, %7, %8}, p;\n\t}" ::"r"(tmem_d),
+        "l"(desc_a), "l"(desc_b), "r"(idesc), "r"(accumulate), "r"(m0), "r"(m1), "r"(m2), "r"(m3)
+        : "memory");
+}
+
+// mbarrier arrive that also sets the expected transaction bytes (TMA / bulk copies).
+QRM_D void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n\t}" ::"r"(
+                     smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+
+// 4-D TMA tile load global -> shared, completion on an mbarrier (tx bytes).
+QRM_D void tma_load_4d(uint32_t dst_smem, const void* tmap, int c0, int c1, int c2, int c3, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, "
+        "%5}], [%6];" ::"r"(dst_smem),
+        "l"(tmap), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar))
+        : "memory");
+}
+
+// Contiguous bulk copy global -> shared (bytes % 16 == 0), completion on an mbarrier.
+QRM_D void bulk_load(uint32_t dst_smem, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst_smem),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
 // Arrive (once) on an mbarrier when all previously issued tcgen05.mma of this
 // thread have completed. Implies tcgen05.fence::before_thread_sync.
 QRM_D void umma_commit(uint64_t* bar) {
@@ -191,6 +228,13 @@ QRM_D uint64_t sw128_kmajor_desc(uint32_t smem_addr) {
     d |= static_cast<uint64_t>(1) << 46;                    // descriptor version (sm_100)
     d |= static_cast<uint64_t>(2) << 61;                    // SWIZZLE_128B
     return d;
+}
+
+// Same, for a view that starts at an arbitrary 128-byte row of the swizzle
+// pattern: the base-offset field carries (start >> 7) & 7 so the hardware
+// applies the XOR pattern the producer (TMA) wrote with.
+QRM_D uint64_t sw128_kmajor_desc_any(uint32_t smem_addr) {
+    return sw128_kmajor_desc(smem_addr) | (static_cast<uint64_t>((smem_addr >> 7) & 7) << 49);
 }
 
 // Instruction descriptor (kind::i8): D s32, A u8, B s8, both K-major.
