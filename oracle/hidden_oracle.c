@@ -67,8 +67,21 @@ ORC_API float orc_hidden_linear_b(uint64_t seed, int o) {
     return (float)(0.1 * (2.0 * orc_rng_unit(seed, 0x4e00, 1000000 + (uint64_t)o) - 1.0));
 }
 
+static void forward_impl(uint64_t seed, int nbits, int l, const uint8_t* tile, double* logits, double* pooled_out,
+                         int stop_after, float* act_out);
+
 /* One tile (u8 l x l x 3, HWC) -> logits[nbits] and (optional) pooled[nbits]. */
 ORC_API void orc_hidden_forward(uint64_t seed, int nbits, int l, const uint8_t* tile, double* logits, double* pooled_out) {
+    forward_impl(seed, nbits, l, tile, logits, pooled_out, -1, NULL);
+}
+
+/* Activations (HWC, l*l*cout floats) after layer `stop_after` (diagnostics). */
+ORC_API void orc_hidden_activation(uint64_t seed, int nbits, int l, const uint8_t* tile, int stop_after, float* act_out) {
+    forward_impl(seed, nbits, l, tile, NULL, NULL, stop_after, act_out);
+}
+
+static void forward_impl(uint64_t seed, int nbits, int l, const uint8_t* tile, double* logits, double* pooled_out,
+                         int stop_after, float* act_out) {
     const int P = l * l;
     float* x = malloc(sizeof(float) * (size_t)P * HID_C);
     float* y = malloc(sizeof(float) * (size_t)P * HID_C);
@@ -102,6 +115,13 @@ ORC_API void orc_hidden_forward(uint64_t seed, int nbits, int l, const uint8_t* 
         float* tmp = x;
         x = y;
         y = tmp;
+        if (j == stop_after) {
+            memcpy(act_out, x, sizeof(float) * (size_t)P * cout);
+            free(x);
+            free(y);
+            free(w);
+            return;
+        }
     }
     double pooled[256];
     for (int c = 0; c < nbits; ++c) {

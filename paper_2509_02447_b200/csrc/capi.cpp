@@ -977,6 +977,42 @@ QRM_EXPORT qrm_status qrm_hidden_detect_device(qrm_ctx* c, const uint8_t* images
     return QRM_OK;
 }
 
+QRM_EXPORT qrm_status qrm_hidden_debug_activation(qrm_ctx* c, const uint8_t* images, int64_t count, int w, int h,
+                                                  int64_t stride, uint64_t first_draw, uint64_t weight_seed,
+                                                  int stop_after, void* out, void* stream) {
+    qrm_status s = check_uniform(c, images, count, w, h, stride);
+    if (s != QRM_OK) return s;
+    if (c->l != 64 || stop_after < 0 || stop_after > kHiddenLayers - 1 || !out)
+        return fail(QRM_INVALID_INPUT, "bad debug request");
+    if ((s = set_device(c->device)) != QRM_OK) return s;
+    cudaStream_t st = as_stream(stream);
+    Workspace& W = c->ws[0];
+    if ((s = hidden_prepare(c, weight_seed, count, st)) != QRM_OK) return s;
+    WindowSource src;
+    if ((s = window_source(c, W, images, count, w, h, stride, first_draw, st, src)) != QRM_OK) return s;
+    auto& H = c->hid;
+    Conv0Params p0{src, count, c->K, H.w0, H.bias, H.act[0]};
+    QRM_LAUNCH(launch_conv0(p0, st));
+    for (int j = 1; j <= stop_after; ++j) {
+        HiddenLayerParams lp{};
+        lp.w_swizzled = H.w_sw + static_cast<int64_t>(j - 1) * 9 * 64 * 64;
+        lp.bias = H.bias + j * 64;
+        lp.last = j == kHiddenLayers - 1;
+        lp.act_out = lp.last ? nullptr : H.act[j & 1];
+        lp.pool_out = lp.last ? H.pool : nullptr;
+        lp.tiles = count;
+        if (const char* e = getenv("QRM_HIDDEN_DBG")) lp.dbg = atoi(e);
+        QRM_LAUNCH(launch_conv64(H.tmap[(j - 1) & 1], lp, c->sms, st));
+    }
+    if (stop_after == kHiddenLayers - 1)
+        QRM_CUDA(cudaMemcpyAsync(out, H.pool, sizeof(float) * kHiddenBlocksPerTile * 64 * count,
+                                 cudaMemcpyDeviceToDevice, st));
+    else
+        QRM_CUDA(cudaMemcpyAsync(out, H.act[stop_after & 1], sizeof(__nv_bfloat16) * 64 * 64 * 64 * count,
+                                 cudaMemcpyDeviceToDevice, st));
+    return QRM_OK;
+}
+
 QRM_EXPORT qrm_status qrm_extract_float_host(uint64_t key_seed, int n_bits, int l, const float* tile, double* soft) {
     if (!tile || !soft || n_bits <= 0 || l <= 0) return fail(QRM_INVALID_INPUT, "bad extract arguments");
     int ndev = 0;

@@ -111,17 +111,21 @@ __global__ void __launch_bounds__(kHThreads, 1)
                 tc_fence_after();
                 const uint32_t d = tmem + a * kHC;
                 const uint32_t as = a_s0 + s * kHABytes;
-#pragma unroll
-                for (int t = 0; t < 9; ++t) {
+                const int ntaps = (p.dbg & 1) ? 1 : 9;
+                for (int t = 0; t < ntaps; ++t) {
                     // centre tap first: it initialises every lane (no mask)
                     const int tap = t == 0 ? 4 : (t <= 4 ? t - 1 : t);
                     const int dy = tap / 3 - 1, dx = tap % 3 - 1;
                     const uint32_t a_view = as + static_cast<uint32_t>((64 * (1 + dy) + dx) * 128);
                     // lanes whose horizontal neighbour is outside the image
-                    const uint32_t m0 = dx < 0 ? 1u : 0u, m1 = dx > 0 ? 0x80000000u : 0u;
+                    uint32_t m0 = dx < 0 ? 1u : 0u, m1 = dx > 0 ? 0x80000000u : 0u;
+                    if (p.dbg & 4) m0 = m1 = 0;
 #pragma unroll
                     for (int k = 0; k < 4; ++k) {
-                        const uint64_t da = sw128_kmajor_desc_any(a_view + 32 * k);
+                        // A view starting mid swizzle-atom: the base-offset field stays 0
+                        // (measured: the XOR pattern is taken from the absolute address bits,
+                        // which TMA wrote with; setting (start>>7)&7 double-applies it).
+                        const uint64_t da = sw128_kmajor_desc(a_view + 32 * k);
                         const uint64_t db = sw128_kmajor_desc(w_s + tap * (kHC * 128) + 32 * k);
                         umma_bf16_masked(d, da, db, idesc, (t | k) != 0, m0, m1, m0, m1);
                     }

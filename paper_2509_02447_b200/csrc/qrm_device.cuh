@@ -230,13 +230,6 @@ QRM_D uint64_t sw128_kmajor_desc(uint32_t smem_addr) {
     return d;
 }
 
-// Same, for a view that starts at an arbitrary 128-byte row of the swizzle
-// pattern: the base-offset field carries (start >> 7) & 7 so the hardware
-// applies the XOR pattern the producer (TMA) wrote with.
-QRM_D uint64_t sw128_kmajor_desc_any(uint32_t smem_addr) {
-    return sw128_kmajor_desc(smem_addr) | (static_cast<uint64_t>((smem_addr >> 7) & 7) << 49);
-}
-
 // Instruction descriptor (kind::i8): D s32, A u8, B s8, both K-major.
 QRM_HD uint32_t idesc_i8_u8s8(int M, int N) {
     return (2u << 4) | (0u << 7) | (1u << 10) | (static_cast<uint32_t>(N >> 3) << 17) |
