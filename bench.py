@@ -147,6 +147,38 @@ def run_reference_arm(args):
     return 0
 
 
+HIDDEN_FLOP_PER_TILE = 2 * 64 * 64 * (27 * 64 + 7 * 576 * 64 + 576 * 60) + 2 * 60 * 60
+
+
+def hidden_submetric(ctx, pool, world, max_over_ranks, stream, batch=BATCH, reps=5):
+    """Learned conv extractor on one device-resident batch: tiles/s and tensor-pipe fraction."""
+    import torch
+
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        peak, kind = float(p["bf16_tflops"]), "measured burst"
+    except Exception:
+        peak, kind = 2250.0, "fallback (nominal dense bf16)"
+    imgs = pool[:batch]
+    for _ in range(3):
+        ctx.hidden_detect_device(imgs, logits=False)
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    for _ in range(reps):
+        ctx.hidden_detect_device(imgs, logits=False)
+    b.record(stream)
+    torch.cuda.synchronize()
+    ms = max_over_ranks(a.elapsed_time(b) / reps)
+    tflops = HIDDEN_FLOP_PER_TILE * batch / (ms / 1e3) / 1e12
+    return {"tiles_per_s": world * batch / (ms / 1e3), "ms_per_batch": ms, "batch": batch,
+            "arch": "9 x (conv3x3 + BN + ReLU) 64ch @ 64x64, avgpool, linear 60x60, RS gf16-15-12",
+            "flop_per_tile": HIDDEN_FLOP_PER_TILE,
+            "roofline": {"bound": "tensor", "achieved": tflops, "peak": peak, "unit": "TFLOP/s",
+                         "frac": tflops / peak, "peak_kind": kind}}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -295,6 +327,15 @@ def main():
                     "achieved_gbs": 17 * args.rs_words / (rms / 1e3) / 1e9}
     small = ne_true <= code.t
     assert bool((ne[small] == ne_true[small]).all())
+    del words, cw, ne, msg
+
+    # Learned extractor (SURVEY 8(d) "learned path"): 9 x conv3x3 64ch on
+    # tcgen05 kind::f16 + pool + head + RS, same 4096-image batches.
+    hidden = None
+    try:
+        hidden = hidden_submetric(ctx, pool, world, max_over_ranks, stream)
+    except Exception as exc:
+        hidden = {"unavailable": str(exc)}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -332,6 +373,7 @@ def main():
                          "kernel_ms": kern_ms, "peak_kind": peak_kind,
                          "algorithmic_bytes_per_launch": alg_bytes},
             "rs": {"words": args.rs_words, "profile": "gf16-15-12", **rs},
+            "learned_extractor": hidden,
             "cpu_baseline": cpu,
             "clocks": clocks.summary(),
         }

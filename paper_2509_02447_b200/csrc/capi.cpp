@@ -38,8 +38,8 @@ namespace qrm {
 cudaError_t launch_corr_detect(const DetectParams& p, int sm_count, cudaStream_t st);
 cudaError_t launch_detect_finish(const DetectParams& p, int tmax, int sm_count, cudaStream_t st);
 cudaError_t launch_gather_windows(const GatherDesc* descs, int64_t count, int l, uint8_t* out, cudaStream_t st);
-cudaError_t launch_rs_packed(const RsTables* tab, int t, int algo, const uint64_t* words, int64_t count, uint64_t* cw,
-                             int8_t* nerr, int sm_count, cudaStream_t st);
+cudaError_t launch_rs_packed(const RsTables* tab, int m, int r, int t, int algo, const uint64_t* words,
+                             int64_t count, uint64_t* cw, int8_t* nerr, int sm_count, cudaStream_t st);
 cudaError_t launch_rs_symbols(const RsTables* tab, int n, int t, const uint8_t* recv, int64_t count, uint8_t* cw,
                               int8_t* nerr, int sm_count, cudaStream_t st);
 cudaError_t launch_rs_stress(const RsTables* tab, const uint64_t* enc_mask, uint64_t seed, int64_t count,
@@ -173,7 +173,8 @@ struct qrm_ctx {
         float *bias = nullptr, *w0 = nullptr, *wl = nullptr, *bl = nullptr, *pool = nullptr;
         __nv_bfloat16* act[2] = {nullptr, nullptr};
         int64_t tiles_cap = 0;
-        CUtensorMap tmap[2];
+        CUtensorMap tmap[2];     // 4-D load maps (conv input)
+        CUtensorMap tmap_st[2];  // 2-D store maps (conv output)
     } hid;
 };
 
@@ -783,7 +784,7 @@ QRM_EXPORT qrm_status qrm_rs_decode_packed_device(int m, int n, int k, const uin
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    QRM_LAUNCH(launch_rs_packed(tab, t, algo, words, count, cw_out, nerr_out, sms, as_stream(stream)));
+    QRM_LAUNCH(launch_rs_packed(tab, m, n - k, t, algo, words, count, cw_out, nerr_out, sms, as_stream(stream)));
     return QRM_OK;
 }
 
@@ -871,7 +872,7 @@ QRM_EXPORT qrm_status qrm_make_corpus_device(const qrm_config* cfg, uint64_t fir
 namespace {
 
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda).
-qrm_status encode_act_tmap(CUtensorMap* map, void* base, int64_t tiles) {
+qrm_status encode_act_tmap(CUtensorMap* map, CUtensorMap* store_map, void* base, int64_t tiles) {
     static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
     if (!encode) {
         cudaDriverEntryPointQueryResult q;
@@ -889,6 +890,15 @@ qrm_status encode_act_tmap(CUtensorMap* map, void* base, int64_t tiles) {
                               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return fail(QRM_CUDA_ERROR, "cuTensorMapEncodeTiled failed (" + std::to_string(r) + ")");
+    // store view of the same buffer: [T*4096 pixels][64 c]; box = 32 pixels (one
+    // epilogue warp's slab), written from a 128B-swizzled staging slab
+    const cuuint64_t sdims[2] = {64, static_cast<cuuint64_t>(tiles) * 4096};
+    const cuuint64_t sstrides[1] = {64 * 2};
+    const cuuint32_t sbox[2] = {64, 32};
+    const CUresult r2 = encode(store_map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, base, sdims, sstrides, sbox, estr,
+                               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                               CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r2 != CUDA_SUCCESS) return fail(QRM_CUDA_ERROR, "cuTensorMapEncodeTiled (store) failed (" + std::to_string(r2) + ")");
     return QRM_OK;
 }
 
@@ -897,7 +907,7 @@ qrm_status hidden_prepare(qrm_ctx* c, uint64_t seed, int64_t tiles, cudaStream_t
     if (!H.w_sw) {
         QRM_CUDA(cudaMalloc(&H.w_sw, sizeof(__nv_bfloat16) * 8 * 9 * 64 * 64));
         QRM_CUDA(cudaMalloc(&H.bias, sizeof(float) * 9 * 64));
-        QRM_CUDA(cudaMalloc(&H.w0, sizeof(float) * 27 * 64));
+        QRM_CUDA(cudaMalloc(&H.w0, sizeof(float) * 64 * 32));
         QRM_CUDA(cudaMalloc(&H.wl, sizeof(float) * 64 * 64));
         QRM_CUDA(cudaMalloc(&H.bl, sizeof(float) * 64));
     }
@@ -915,7 +925,7 @@ qrm_status hidden_prepare(qrm_ctx* c, uint64_t seed, int64_t tiles, cudaStream_t
         QRM_CUDA(cudaMalloc(&H.pool, sizeof(float) * kHiddenBlocksPerTile * 64 * tiles));
         qrm_status s;
         for (int i = 0; i < 2; ++i)
-            if ((s = encode_act_tmap(&H.tmap[i], H.act[i], tiles)) != QRM_OK) return s;
+            if ((s = encode_act_tmap(&H.tmap[i], &H.tmap_st[i], H.act[i], tiles)) != QRM_OK) return s;
         H.tiles_cap = tiles;
     }
     return QRM_OK;
@@ -932,6 +942,7 @@ QRM_EXPORT qrm_status qrm_hidden_detect_device(qrm_ctx* c, const uint8_t* images
     if (s != QRM_OK) return s;
     if (count > 0 && !out) return fail(QRM_INVALID_INPUT, "null record buffer");
     if (c->l != 64) return fail(QRM_INVALID_INPUT, "the conv extractor is defined on 64x64 tiles");
+    if (count >= (int64_t{1} << 19)) return fail(QRM_INVALID_INPUT, "conv extractor batch must be < 524288 tiles");
     if ((s = set_device(c->device)) != QRM_OK) return s;
     if (count == 0) return QRM_OK;
     cudaStream_t st = as_stream(stream);
@@ -942,7 +953,7 @@ QRM_EXPORT qrm_status qrm_hidden_detect_device(qrm_ctx* c, const uint8_t* images
     if ((s = window_source(c, W, images, count, w, h, stride, first_draw, st, src)) != QRM_OK) return s;
     auto& H = c->hid;
     Conv0Params p0{src, count, c->K, H.w0, H.bias, H.act[0]};
-    QRM_LAUNCH(launch_conv0(p0, st));
+    QRM_LAUNCH(launch_conv0(p0, H.tmap_st[0], st));
     for (int j = 1; j < kHiddenLayers; ++j) {
         HiddenLayerParams lp{};
         lp.w_swizzled = H.w_sw + static_cast<int64_t>(j - 1) * 9 * 64 * 64;
@@ -951,7 +962,7 @@ QRM_EXPORT qrm_status qrm_hidden_detect_device(qrm_ctx* c, const uint8_t* images
         lp.act_out = lp.last ? nullptr : H.act[j & 1];
         lp.pool_out = lp.last ? H.pool : nullptr;
         lp.tiles = count;
-        QRM_LAUNCH(launch_conv64(H.tmap[(j - 1) & 1], lp, c->sms, st));
+        QRM_LAUNCH(launch_conv64(H.tmap[(j - 1) & 1], H.tmap_st[j & 1], lp, c->sms, st));
     }
     HeadParams hp{};
     hp.pool = H.pool;
@@ -992,7 +1003,7 @@ QRM_EXPORT qrm_status qrm_hidden_debug_activation(qrm_ctx* c, const uint8_t* ima
     if ((s = window_source(c, W, images, count, w, h, stride, first_draw, st, src)) != QRM_OK) return s;
     auto& H = c->hid;
     Conv0Params p0{src, count, c->K, H.w0, H.bias, H.act[0]};
-    QRM_LAUNCH(launch_conv0(p0, st));
+    QRM_LAUNCH(launch_conv0(p0, H.tmap_st[0], st));
     for (int j = 1; j <= stop_after; ++j) {
         HiddenLayerParams lp{};
         lp.w_swizzled = H.w_sw + static_cast<int64_t>(j - 1) * 9 * 64 * 64;
@@ -1002,7 +1013,7 @@ QRM_EXPORT qrm_status qrm_hidden_debug_activation(qrm_ctx* c, const uint8_t* ima
         lp.pool_out = lp.last ? H.pool : nullptr;
         lp.tiles = count;
         if (const char* e = getenv("QRM_HIDDEN_DBG")) lp.dbg = atoi(e);
-        QRM_LAUNCH(launch_conv64(H.tmap[(j - 1) & 1], lp, c->sms, st));
+        QRM_LAUNCH(launch_conv64(H.tmap[(j - 1) & 1], H.tmap_st[j & 1], lp, c->sms, st));
     }
     if (stop_after == kHiddenLayers - 1)
         QRM_CUDA(cudaMemcpyAsync(out, H.pool, sizeof(float) * kHiddenBlocksPerTile * 64 * count,

@@ -12,13 +12,16 @@
 // it needs (32 KB, rows outside the image zero-filled by TMA) into a
 // 128B-swizzled buffer whose 128-byte rows are pixels (64 bf16 channels). Each
 // of the 9 taps is then a *shifted view* of that buffer (descriptor start at
-// pixel 64(1+dy)+dx, base-offset set for the swizzle phase); the two pixels
-// per row whose horizontal neighbour falls outside the image are excluded
-// with tcgen05.mma's disable-output-lane mask. The 9 taps x 4 K-steps = 36
-// MMAs (M=128, N=64, K=16) accumulate into one of two TMEM buffers while 4
-// epilogue warps drain the other (bias + ReLU -> bf16 NHWC, or, for the last
-// layer, the per-block channel sums of the average pool). All 9 taps of folded
-// weights (72 KB) stay resident in shared memory.
+// pixel 64(1+dy)+dx, base-offset field 0: the swizzle XOR is taken from the
+// absolute address bits); the two pixels per row whose horizontal neighbour
+// falls outside the image are excluded with tcgen05.mma's disable-output-lane
+// mask. The 9 taps x 4 K-steps = 36 MMAs (M=128, N=64, K=16) accumulate into
+// one of two TMEM buffers while 4 epilogue warps drain the other: bias + ReLU
+// -> bf16 rows written 128B-swizzled (bank-conflict free) into a 4 KB staging
+// slab per warp and stored by one TMA tensor store per warp (32 contiguous
+// NHWC pixels), or, for the last layer, the per-block channel sums of the
+// average pool. All 9 taps of folded weights (72 KB) stay resident in shared
+// memory; the A ring is 4 stages deep.
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -38,7 +41,7 @@ constexpr int kHM = 128;                   // pixels per output block (2 rows)
 constexpr int kHBlocks = kHPix / kHM;      // 32 blocks per tile
 constexpr int kHWBytes = 9 * kHC * kHC * 2;  // 73,728 B of bf16 weights per layer
 constexpr int kHABytes = 4 * kHSide * kHC * 2;  // 32 KB: 4 input rows
-constexpr int kHAStages = 2;
+constexpr int kHAStages = 4;
 constexpr int kHThreads = 192;             // warp 0 TMA, warp 1 MMA, warps 2-5 epilogue
 
 struct HiddenSmem {
@@ -49,17 +52,21 @@ struct HiddenSmem {
     float bias[kHC];
     float pool[4][kHC];  // per-epilogue-warp channel sums (last layer)
 };
-// layout: [W 72 KB][A0 32 KB][A1 32 KB][HiddenSmem] (+1 KB align slack, views may
-// read <= 128 B outside an A buffer; those rows are masked lanes)
-constexpr size_t kHSmemBytes = 1024 + kHWBytes + kHAStages * kHABytes + 1024;
+constexpr int kHOBytes = 4 * 32 * kHC * 2;  // 16 KB: output staging, 4 KB per epilogue warp
+// layout: [W 72 KB][A0..A3 4 x 32 KB][O 16 KB][128 B][HiddenSmem] (+1 KB align
+// slack; views may read <= 128 B outside an A buffer; those rows are masked lanes)
+constexpr size_t kHSmemBytes = 1024 + kHWBytes + kHAStages * kHABytes + kHOBytes + 128 + sizeof(HiddenSmem);
+static_assert(kHSmemBytes <= 232448, "conv64 shared memory exceeds 227 KB");
 
 __global__ void __launch_bounds__(kHThreads, 1)
-    conv64_kernel(const __grid_constant__ CUtensorMap tmap_in, const __grid_constant__ HiddenLayerParams p) {
+    conv64_kernel(const __grid_constant__ CUtensorMap tmap_in, const __grid_constant__ CUtensorMap tmap_out,
+                  const __grid_constant__ HiddenLayerParams p) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const uint32_t w_s = smem_u32(base);
     const uint32_t a_s0 = w_s + kHWBytes;
-    HiddenSmem& sm = *reinterpret_cast<HiddenSmem*>(base + kHWBytes + kHAStages * kHABytes + 128);
+    const uint32_t o_s = a_s0 + kHAStages * kHABytes;
+    HiddenSmem& sm = *reinterpret_cast<HiddenSmem*>(base + kHWBytes + kHAStages * kHABytes + kHOBytes + 128);
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int64_t nblocks = p.tiles * kHBlocks;
@@ -100,41 +107,44 @@ __global__ void __launch_bounds__(kHThreads, 1)
         }
     } else if (warp == 1) {
         // ---------------------------------------------------------- MMA ----
-        if (lane == 0) {
-            const uint32_t idesc = idesc_bf16_f32(kHM, kHC);
-            mbar_wait(&sm.w_full, 0);
-            int i = 0;
-            for (int64_t b = blockIdx.x; b < nblocks; b += gridDim.x, ++i) {
-                const int s = i % kHAStages, a = i & 1;
-                mbar_wait(&sm.a_full[s], (i / kHAStages) & 1);
-                mbar_wait(&sm.acc_empty[a], ((i >> 1) & 1) ^ 1);
-                tc_fence_after();
-                const uint32_t d = tmem + a * kHC;
-                const uint32_t as = a_s0 + s * kHABytes;
-                const int ntaps = (p.dbg & 1) ? 1 : 9;
-                for (int t = 0; t < ntaps; ++t) {
+        // The whole warp runs the loop (uniform control flow); one elected lane
+        // issues. Descriptors are a per-block base plus compile-time offsets.
+        const uint32_t idesc = idesc_bf16_f32(kHM, kHC);
+        const uint64_t db0 = sw128_kmajor_desc(w_s);
+        const bool aligned_views = (p.dbg & 8) != 0;  // timing experiment only (wrong math)
+        mbar_wait(&sm.w_full, 0);
+        int i = 0;
+        for (int64_t b = blockIdx.x; b < nblocks; b += gridDim.x, ++i) {
+            const int s = i % kHAStages, a = i & 1;
+            mbar_wait(&sm.a_full[s], (i / kHAStages) & 1);
+            mbar_wait(&sm.acc_empty[a], ((i >> 1) & 1) ^ 1);
+            tc_fence_after();
+            const uint32_t d = tmem + a * kHC;
+            const uint64_t da0 = sw128_kmajor_desc(a_s0 + s * kHABytes);
+            if (elect_one()) {
+#pragma unroll
+                for (int t = 0; t < 9; ++t) {
                     // centre tap first: it initialises every lane (no mask)
                     const int tap = t == 0 ? 4 : (t <= 4 ? t - 1 : t);
                     const int dy = tap / 3 - 1, dx = tap % 3 - 1;
-                    const uint32_t a_view = as + static_cast<uint32_t>((64 * (1 + dy) + dx) * 128);
+                    // A view: pixel row 64(1+dy)+dx of the 4-row buffer. It may start mid
+                    // swizzle-atom; the base-offset field stays 0 (measured: the XOR
+                    // pattern is taken from the absolute address bits TMA wrote with).
+                    const int view = aligned_views ? 64 * 128 : (64 * (1 + dy) + dx) * 128;
                     // lanes whose horizontal neighbour is outside the image
-                    uint32_t m0 = dx < 0 ? 1u : 0u, m1 = dx > 0 ? 0x80000000u : 0u;
-                    if (p.dbg & 4) m0 = m1 = 0;
+                    const uint32_t m0 = dx < 0 ? 1u : 0u, m1 = dx > 0 ? 0x80000000u : 0u;
 #pragma unroll
                     for (int k = 0; k < 4; ++k) {
-                        // A view starting mid swizzle-atom: the base-offset field stays 0
-                        // (measured: the XOR pattern is taken from the absolute address bits,
-                        // which TMA wrote with; setting (start>>7)&7 double-applies it).
-                        const uint64_t da = sw128_kmajor_desc(a_view + 32 * k);
-                        const uint64_t db = sw128_kmajor_desc(w_s + tap * (kHC * 128) + 32 * k);
+                        const uint64_t da = da0 + static_cast<uint64_t>(static_cast<int64_t>((view + 32 * k) >> 4));
+                        const uint64_t db = db0 + static_cast<uint64_t>((tap * (kHC * 128) + 32 * k) >> 4);
                         umma_bf16_masked(d, da, db, idesc, (t | k) != 0, m0, m1, m0, m1);
                     }
                 }
                 umma_commit(&sm.a_empty[s]);
                 umma_commit(&sm.acc_full[a]);
             }
+            __syncwarp();
         }
-        __syncwarp();
     } else {
         // ----------------------------------------------------- epilogue ----
         const int q = warp & 3;  // TMEM lane quarter this warp may access
@@ -161,7 +171,13 @@ __global__ void __launch_bounds__(kHThreads, 1)
 #pragma unroll
             for (int c = 0; c < kHC; ++c) v[c] = fmaxf(__uint_as_float(acc[c]) + sm.bias[c], 0.0f);
             if (!p.last) {
-                uint4* dst = reinterpret_cast<uint4*>(p.act_out + (tile * kHPix + pix) * kHC);
+                // Stage this warp's 32 pixels x 128 B as a 128B-swizzled slab (16-B
+                // chunk c of row r at chunk c ^ (r & 7): conflict free), then one TMA
+                // store writes the 4 KB contiguous NHWC run.
+                const uint32_t slab = o_s + q * 4096;
+                if (lane == 0) bulk_wait_read<0>();  // previous store has read the slab
+                __syncwarp();
+                const uint32_t row = slab + lane * 128;
 #pragma unroll
                 for (int c = 0; c < kHC; c += 8) {
                     uint4 o;
@@ -173,7 +189,13 @@ __global__ void __launch_bounds__(kHThreads, 1)
                     o.y = *reinterpret_cast<uint32_t*>(&h1);
                     o.z = *reinterpret_cast<uint32_t*>(&h2);
                     o.w = *reinterpret_cast<uint32_t*>(&h3);
-                    dst[c / 8] = o;
+                    st_shared_v4(row + ((((c >> 3) ^ lane) & 7) << 4), o);
+                }
+                fence_proxy_async_smem();
+                __syncwarp();
+                if (lane == 0) {
+                    tma_store_2d(&tmap_out, slab, 0, static_cast<int>(tile * kHPix + pix - lane));
+                    bulk_commit();
                 }
             } else {
                 // Average pool, part 1: channel sums over this warp's 32 pixels by
@@ -202,6 +224,7 @@ __global__ void __launch_bounds__(kHThreads, 1)
                 asm volatile("bar.sync 1, 128;" ::: "memory");
             }
         }
+        if (!p.last && lane == 0) bulk_wait<0>();
     }
     __syncthreads();
     if (warp == 1) {
@@ -210,55 +233,132 @@ __global__ void __launch_bounds__(kHThreads, 1)
     }
 }
 
-// First layer (3 -> 64, K = 27): on CUDA cores (0.6% of the stack's FLOPs).
-// One thread per pixel; the normalised input window comes straight from the
-// image (same tile selection as the correlation decoder).
-__global__ void __launch_bounds__(128) conv0_kernel(const __grid_constant__ Conv0Params p) {
-    __shared__ float w[27 * kHC];
+// First layer (3 -> 64, K = 27) as one tcgen05 kind::tf32 GEMM per 128-pixel
+// block: D[128 px][64 co] = A[128 px][32] . W0[64 co][32]^T, K = 27 taps x
+// channels zero-padded to 32 (fp32 rows of exactly 128 B, one 128B-swizzle
+// atom row). The CTA stages the block's 4 input rows (u8) in shared memory,
+// each thread builds its pixel's im2col row from a 256-entry normalisation
+// table (float(v/127.5 - 1), image.cpp:36, rounded to tf32) and one thread
+// issues the 4 MMAs (K = 8 each). Epilogue as conv64: bias + ReLU -> bf16 rows
+// 128B-swizzled into a per-warp staging slab -> one TMA store per warp. Small
+// CTAs (24 KB smem, 64 TMEM columns) so several blocks overlap per SM.
+constexpr int kC0Threads = 128;
+constexpr int kC0K = 32;  // padded K (fp32 elements per A/B row)
+
+__global__ void __launch_bounds__(kC0Threads) conv0_kernel(const __grid_constant__ CUtensorMap tmap_out,
+                                                           const __grid_constant__ Conv0Params p) {
+    __shared__ __align__(1024) uint8_t a_tile[kHM * kC0K * 4];  // 16 KB A (reused as output staging)
+    __shared__ __align__(1024) uint8_t b_tile[kHC * kC0K * 4];  // 8 KB W0 (pre-swizzled)
+    __shared__ float lut[256];
     __shared__ float bsh[kHC];
-    for (int i = threadIdx.x; i < 27 * kHC; i += blockDim.x) w[i] = p.w0[i];
-    if (threadIdx.x < kHC) bsh[threadIdx.x] = p.b0[threadIdx.x];
-    __syncthreads();
+    __shared__ uint8_t rows[4][3 * kHSide];
+    __shared__ uint64_t done;
+    __shared__ uint32_t tmem_slot;
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int64_t tile = blockIdx.x / kHBlocks;
-    if (tile >= p.tiles) return;
-    const int pix = static_cast<int>(blockIdx.x % kHBlocks) * kHM + threadIdx.x;
-    const int py = pix / kHSide, px = pix % kHSide;
+    const int blk = static_cast<int>(blockIdx.x % kHBlocks);
+    if (warp == 0) tmem_alloc<kHC>(&tmem_slot);
+    if (tid == 0) {
+        mbar_init(&done, 1);
+        mbar_fence_init();
+    }
+    // normalisation table, exactly float(v/127.5 - 1.0) then tf32-rounded
+    for (int v = tid; v < 256; v += kC0Threads) {
+        const float f = __double2float_rn(static_cast<double>(v) / 127.5 - 1.0);
+        uint32_t t;
+        asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(t) : "f"(f));
+        lut[v] = __uint_as_float(t);
+    }
+    if (tid < kHC) bsh[tid] = p.b0[tid];
+    {
+        const uint4* src = reinterpret_cast<const uint4*>(p.w0);
+        uint4* dst = reinterpret_cast<uint4*>(b_tile);
+#pragma unroll
+        for (int i = 0; i < (kHC * kC0K * 4) / 16 / kC0Threads; ++i)
+            dst[tid + i * kC0Threads] = __ldg(src + tid + i * kC0Threads);
+    }
+    // the 4 input rows y0-1 .. y0+2 (zero outside the tile)
     const uint8_t* wb = window_base(p.src, tile, p.K);
     const int pitch = p.src.direct ? p.src.pitch : 3 * kHSide;
-    float x[27];
-#pragma unroll
-    for (int t = 0; t < 9; ++t) {
-        const int sy = py + t / 3 - 1, sx = px + t % 3 - 1;
-        const bool in = sy >= 0 && sy < kHSide && sx >= 0 && sx < kHSide;
-#pragma unroll
-        for (int c = 0; c < 3; ++c) {
-            // float(v/127.5 - 1) exactly as normalize (image.cpp:36)
-            x[t * 3 + c] = in ? __double2float_rn(__dsub_rn(
-                                    __ddiv_rn(static_cast<double>(wb[static_cast<int64_t>(sy) * pitch + sx * 3 + c]),
-                                              127.5),
-                                    1.0))
-                              : 0.0f;
-        }
+    const int y0 = blk * 2;
+    for (int i = tid; i < 4 * 3 * kHSide; i += kC0Threads) {
+        const int r = i / (3 * kHSide), x = i - r * (3 * kHSide);
+        const int sy = y0 - 1 + r;
+        rows[r][x] = (sy >= 0 && sy < kHSide) ? wb[static_cast<int64_t>(sy) * pitch + x] : uint8_t{0};
     }
-    __nv_bfloat16* dst = p.act_out + (tile * kHPix + pix) * kHC;
+    __syncthreads();
+
+    // im2col row of pixel (y0 + tid/64, tid%64): k = tap*3 + c, tap = 3(dy+1) + (dx+1)
+    {
+        const int ry = 1 + (tid >> 6), px = tid & 63;
+        float x[kC0K];
 #pragma unroll
-    for (int c0 = 0; c0 < kHC; c0 += 8) {
-        float o[8];
+        for (int t = 0; t < 9; ++t) {
+            const int sx = px + t % 3 - 1;
+            const bool in = sx >= 0 && sx < kHSide;
+            const uint8_t* rp = rows[ry + t / 3 - 1];
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-            float s = bsh[c0 + j];
-#pragma unroll
-            for (int k = 0; k < 27; ++k) s = fmaf(x[k], w[k * kHC + c0 + j], s);
-            o[j] = fmaxf(s, 0.0f);
+            for (int c = 0; c < 3; ++c) x[t * 3 + c] = in ? lut[rp[sx * 3 + c]] : 0.0f;
         }
-        uint4 u;
-        __nv_bfloat162 h0 = __floats2bfloat162_rn(o[0], o[1]), h1 = __floats2bfloat162_rn(o[2], o[3]);
-        __nv_bfloat162 h2 = __floats2bfloat162_rn(o[4], o[5]), h3 = __floats2bfloat162_rn(o[6], o[7]);
-        u.x = *reinterpret_cast<uint32_t*>(&h0);
-        u.y = *reinterpret_cast<uint32_t*>(&h1);
-        u.z = *reinterpret_cast<uint32_t*>(&h2);
-        u.w = *reinterpret_cast<uint32_t*>(&h3);
-        reinterpret_cast<uint4*>(dst)[c0 / 8] = u;
+#pragma unroll
+        for (int k = 27; k < kC0K; ++k) x[k] = 0.0f;
+        const uint32_t row = smem_u32(a_tile) + tid * 128;
+#pragma unroll
+        for (int c = 0; c < 8; ++c)
+            st_shared_v4(row + (((c ^ tid) & 7) << 4),
+                         make_uint4(__float_as_uint(x[4 * c]), __float_as_uint(x[4 * c + 1]),
+                                    __float_as_uint(x[4 * c + 2]), __float_as_uint(x[4 * c + 3])));
+    }
+    fence_proxy_async_smem();  // generic-proxy writes of A and B -> visible to the tensor core
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = tmem_slot;
+    if (tid == 0) {
+        const uint32_t idesc = idesc_tf32_f32(kHM, kHC);
+        const uint64_t da = sw128_kmajor_desc(smem_u32(a_tile)), db = sw128_kmajor_desc(smem_u32(b_tile));
+#pragma unroll
+        for (int k = 0; k < kC0K / 8; ++k) umma_tf32(tmem, da + 2 * k, db + 2 * k, idesc, k != 0);
+        umma_commit(&done);
+    }
+    mbar_wait(&done, 0);
+    tc_fence_after();
+    uint32_t acc[kHC];
+#pragma unroll
+    for (int c = 0; c < kHC / 16; ++c) {
+        uint32_t r16[16];
+        tmem_ld16(tmem + (static_cast<uint32_t>(warp * 32) << 16) + c * 16, r16);
+#pragma unroll
+        for (int j = 0; j < 16; ++j) acc[c * 16 + j] = r16[j];
+    }
+    tmem_ld_wait();
+    // the MMAs completed (done), so A is free: stage the bf16 output rows in it
+    const uint32_t slab = smem_u32(a_tile) + warp * 4096;
+    const uint32_t row = slab + lane * 128;
+#pragma unroll
+    for (int c = 0; c < kHC; c += 8) {
+        float v[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) v[j] = fmaxf(__uint_as_float(acc[c + j]) + bsh[c + j], 0.0f);
+        __nv_bfloat162 h0 = __floats2bfloat162_rn(v[0], v[1]), h1 = __floats2bfloat162_rn(v[2], v[3]);
+        __nv_bfloat162 h2 = __floats2bfloat162_rn(v[4], v[5]), h3 = __floats2bfloat162_rn(v[6], v[7]);
+        st_shared_v4(row + ((((c >> 3) ^ lane) & 7) << 4),
+                     make_uint4(*reinterpret_cast<uint32_t*>(&h0), *reinterpret_cast<uint32_t*>(&h1),
+                                *reinterpret_cast<uint32_t*>(&h2), *reinterpret_cast<uint32_t*>(&h3)));
+    }
+    fence_proxy_async_smem();
+    __syncwarp();
+    if (lane == 0) {
+        tma_store_2d(&tmap_out, slab, 0, static_cast<int>(tile * kHPix + blk * kHM + warp * 32));
+        bulk_commit();
+        bulk_wait_read<0>();  // the slab must stay valid until the store has read it
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) {
+        tc_fence_after();
+        tmem_dealloc<kHC>(tmem);
     }
 }
 
@@ -356,9 +456,13 @@ __global__ void hidden_prep_kernel(uint64_t seed, int nbits, __nv_bfloat16* w_sw
     }
     __syncthreads();
     if (j == 0) {
-        for (int i = threadIdx.x; i < 27 * kHC; i += blockDim.x) {
-            const int k = i / kHC, co = i % kHC;
-            w0[i] = hidden_weight(seed, 0, co, k / 3, k % 3) * scale[co];
+        // smem image of the 128B-swizzled K-major [64 co][32 k] fp32 (tf32-rounded) B tile
+        for (int i = threadIdx.x; i < kHC * kC0K; i += blockDim.x) {
+            const int co = i / kC0K, k = i % kC0K;
+            const float val = k < 27 ? hidden_weight(seed, 0, co, k / 3, k % 3) * scale[co] : 0.0f;
+            uint32_t t;
+            asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(t) : "f"(val));
+            w0[co * kC0K + (((k / 4) ^ (co & 7)) * 4) + (k % 4)] = __uint_as_float(t);
         }
         return;
     }
@@ -380,12 +484,13 @@ cudaError_t launch_hidden_prep(uint64_t seed, int nbits, __nv_bfloat16* w_sw, fl
     return cudaGetLastError();
 }
 
-cudaError_t launch_conv0(const Conv0Params& p, cudaStream_t st) {
-    conv0_kernel<<<static_cast<unsigned>(p.tiles * kHBlocks), 128, 0, st>>>(p);
+cudaError_t launch_conv0(const Conv0Params& p, const CUtensorMap& tmap_out, cudaStream_t st) {
+    conv0_kernel<<<static_cast<unsigned>(p.tiles * kHBlocks), kC0Threads, 0, st>>>(tmap_out, p);
     return cudaGetLastError();
 }
 
-cudaError_t launch_conv64(const CUtensorMap& tmap, const HiddenLayerParams& p, int sm_count, cudaStream_t st) {
+cudaError_t launch_conv64(const CUtensorMap& tmap, const CUtensorMap& tmap_out, const HiddenLayerParams& p,
+                          int sm_count, cudaStream_t st) {
     static bool configured = false;
     if (!configured) {
         cudaError_t e = cudaFuncSetAttribute(conv64_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -396,7 +501,7 @@ cudaError_t launch_conv64(const CUtensorMap& tmap, const HiddenLayerParams& p, i
     const int64_t nblocks = p.tiles * kHBlocks;
     int64_t grid = sm_count > 0 ? sm_count : 148;
     if (grid > nblocks) grid = nblocks;
-    conv64_kernel<<<static_cast<unsigned>(grid), kHThreads, kHSmemBytes, st>>>(tmap, p);
+    conv64_kernel<<<static_cast<unsigned>(grid), kHThreads, kHSmemBytes, st>>>(tmap, tmap_out, p);
     return cudaGetLastError();
 }
 

@@ -162,6 +162,15 @@ QRM_D void umma_bf16(uint32_t tmem_d, uint64_t desc_a, uint64_t desc_b, uint32_t
         : "memory");
 }
 
+QRM_D void umma_tf32(uint32_t tmem_d, uint64_t desc_a, uint64_t desc_b, uint32_t idesc, uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(desc_a), "l"(desc_b), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+
 // As umma_bf16, with output lanes disabled (mask bit set = lane not written):
 // mask[q] covers lanes 32q..32q+31.
 QRM_D void umma_bf16_masked(uint32_t tmem_d, uint64_t desc_a, uint64_t desc_b, uint32_t idesc, uint32_t accumulate,
@@ -191,12 +200,44 @@ QRM_D void tma_load_4d(uint32_t dst_smem, const void* tmap, int c0, int c1, int 
         : "memory");
 }
 
+// TMA tensor store shared -> global (bulk-group completion).
+QRM_D void tma_store_2d(const void* tmap, uint32_t src_smem, int c0, int c1) {
+    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(tmap),
+                 "r"(src_smem), "r"(c0), "r"(c1)
+                 : "memory");
+}
+QRM_D void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+// Wait until at most N committed bulk groups still READ their shared source.
+template <int N>
+QRM_D void bulk_wait_read() {
+    asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+template <int N>
+QRM_D void bulk_wait() {
+    asm volatile("cp.async.bulk.wait_group %0;" ::"n"(N) : "memory");
+}
+QRM_D void st_shared_v4(uint32_t addr, uint4 v) {
+    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+                 : "memory");
+}
+
 // Contiguous bulk copy global -> shared (bytes % 16 == 0), completion on an mbarrier.
 QRM_D void bulk_load(uint32_t dst_smem, const void* src, uint32_t bytes, uint64_t* bar) {
     asm volatile(
         "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst_smem),
         "l"(src), "r"(bytes), "r"(smem_u32(bar))
         : "memory");
+}
+
+// One elected lane of a converged warp (elect.sync).
+QRM_D bool elect_one() {
+    uint32_t pred = 0;
+    asm volatile(
+        "{\n\t.reg .pred P;\n\t.reg .b32 r;\n\t"
+        "elect.sync r|P, 0xffffffff;\n\t"
+        "selp.b32 %0, 1, 0, P;\n\t}"
+        : "=r"(pred));
+    return pred != 0;
 }
 
 // Arrive (once) on an mbarrier when all previously issued tcgen05.mma of this
@@ -239,6 +280,12 @@ QRM_HD uint32_t idesc_i8_u8s8(int M, int N) {
 // Instruction descriptor (kind::f16): D f32, A bf16, B bf16, both K-major.
 QRM_HD uint32_t idesc_bf16_f32(int M, int N) {
     return (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(N >> 3) << 17) |
+           (static_cast<uint32_t>(M >> 4) << 24);
+}
+
+// Instruction descriptor (kind::tf32): D f32, A tf32, B tf32, both K-major.
+QRM_HD uint32_t idesc_tf32_f32(int M, int N) {
+    return (1u << 4) | (2u << 7) | (2u << 10) | (static_cast<uint32_t>(N >> 3) << 17) |
            (static_cast<uint32_t>(M >> 4) << 24);
 }
 

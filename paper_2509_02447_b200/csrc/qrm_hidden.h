@@ -27,7 +27,7 @@ struct Conv0Params {
     WindowSource src;
     int64_t tiles;
     int32_t K;
-    const float* w0;  // [27][64] folded, tap-major (tap*3 + ci)
+    const float* w0;  // [64 co][32 k] folded, tf32, 128B-swizzled smem image (k = tap*3 + ci, zero k >= 27)
     const float* b0;  // [64]
     __nv_bfloat16* act_out;
 };
@@ -48,8 +48,11 @@ struct HeadParams {
 
 cudaError_t launch_hidden_prep(uint64_t seed, int nbits, __nv_bfloat16* w_sw, float* bias, float* w0, float* wl,
                                float* bl, cudaStream_t st);
-cudaError_t launch_conv0(const Conv0Params& p, cudaStream_t st);
-cudaError_t launch_conv64(const CUtensorMap& tmap, const HiddenLayerParams& p, int sm_count, cudaStream_t st);
+cudaError_t launch_conv0(const Conv0Params& p, const CUtensorMap& tmap_out, cudaStream_t st);
+// tmap: 4-D load map of the input activations; tmap_out: 2-D store map of the
+// output activations ({64 ch, T*4096 px}, box {64, 32}, 128B swizzle).
+cudaError_t launch_conv64(const CUtensorMap& tmap, const CUtensorMap& tmap_out, const HiddenLayerParams& p,
+                          int sm_count, cudaStream_t st);
 cudaError_t launch_hidden_head(const HeadParams& p, cudaStream_t st);
 
 }  // namespace qrm

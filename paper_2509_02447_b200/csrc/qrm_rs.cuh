@@ -40,6 +40,48 @@ __device__ __forceinline__ uint32_t gf_div(const RsSmem& T, uint32_t a, uint32_t
     return a ? T.exp2[T.log[a] + T.q1 - T.log[b]] : 0u;
 }
 
+// Compile-time form of rs_t1_packed for the batched RS kernels: MB syndrome
+// bits per symbol (4, or 8 for any m <= 8: masks above m are zero) and R = n-k
+// checks, with the R*MB syndrome masks held in registers (mk) and only the
+// log/antilog tables read from shared memory. Same result as rs_t1_packed.
+template <int MB, int R>
+__device__ __forceinline__ int rs_t1_fixed(const RsSmem& T, const uint64_t (&mk)[R * MB], uint64_t word,
+                                           uint64_t& cw) {
+    uint32_t S[R];
+    uint32_t any = 0;
+#pragma unroll
+    for (int j = 0; j < R; ++j) {
+        uint32_t s = 0;
+#pragma unroll
+        for (int e = 0; e < MB; ++e) {
+            // parity of a 64-bit word = parity of its two halves XORed (one POPC)
+            const uint64_t x = word & mk[j * MB + e];
+            s |= static_cast<uint32_t>(__popc(static_cast<uint32_t>(x) ^ static_cast<uint32_t>(x >> 32)) & 1) << e;
+        }
+        S[j] = s;
+        any |= s;
+    }
+    cw = word;
+    if (!any) return 0;
+    if (S[0] == 0 || S[1] == 0) return -1;
+    const int q1 = T.q1;
+    const int l0 = T.log[S[0]];
+    int pos = static_cast<int>(T.log[S[1]]) - l0;
+    if (pos < 0) pos += q1;
+    if (pos >= T.n) return -1;
+    if (R > 2) {
+        if (S[R - 1] == 0) return -1;
+        int want = l0 + 2 * pos;  // < 3 q1
+        if (want >= q1) want -= q1;
+        if (want >= q1) want -= q1;
+        if (static_cast<int>(T.log[S[R - 1]]) != want) return -1;
+    }
+    int le = l0 - static_cast<int>(T.logv[pos]);
+    if (le < 0) le += q1;
+    cw = word ^ (static_cast<uint64_t>(T.exp2[le]) << (T.m * (T.n - 1 - pos)));
+    return 1;
+}
+
 // t = 1 bounded-distance decode of a packed word (n*m <= 64, n-k in {2,3}).
 // Returns errors_corrected (0/1) and the corrected codeword, or -1.
 __device__ __forceinline__ int rs_t1_packed(const RsSmem& T, uint64_t word, uint64_t& cw) {

@@ -27,13 +27,19 @@ __global__ void __launch_bounds__(256) rs_t1_packed_kernel(const RsTables* __res
 
 // Vectorised form: each thread decodes 4 consecutive words (two 16-byte
 // loads issued before any compute, so each thread keeps 32 B in flight);
-// requires 16-byte aligned word arrays and 4-byte aligned nerr.
+// requires 16-byte aligned word arrays and 4-byte aligned nerr. The code shape
+// (MB syndrome bits per symbol, R = n-k) is compile-time and the syndrome
+// masks live in registers.
+template <int MB, int R>
 __global__ void __launch_bounds__(256) rs_t1_packed_x4_kernel(const RsTables* __restrict__ g,
                                                              const ulonglong2* __restrict__ words, int64_t groups,
                                                              ulonglong2* __restrict__ cw_out,
                                                              uint32_t* __restrict__ nerr_out) {
     __shared__ RsSmem T;
     rs_stage_tables(T, g, threadIdx.x, blockDim.x);
+    uint64_t mk[R * MB];
+#pragma unroll
+    for (int j = 0; j < R * MB; ++j) mk[j] = __ldg(&g->synd_mask[j]);
     __syncthreads();
     const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
     for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < groups; i += stride) {
@@ -43,8 +49,8 @@ __global__ void __launch_bounds__(256) rs_t1_packed_x4_kernel(const RsTables* __
         uint32_t ne = 0;
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-            uint64_t cw = 0;
-            const int e = rs_t1_packed(T, w[j], cw);
+            uint64_t cw;
+            const int e = rs_t1_fixed<MB, R>(T, mk, w[j], cw);
             c[j] = e >= 0 ? cw : 0ull;
             ne |= (static_cast<uint32_t>(e) & 0xFFu) << (8 * j);
         }
@@ -152,8 +158,8 @@ __global__ void rs_stress_kernel(const RsTables* __restrict__ g, const uint64_t*
     }
 }
 
-cudaError_t launch_rs_packed(const RsTables* tab, int t, int algo, const uint64_t* words, int64_t count,
-                             uint64_t* cw, int8_t* nerr, int sm_count, cudaStream_t st) {
+cudaError_t launch_rs_packed(const RsTables* tab, int m, int r, int t, int algo, const uint64_t* words,
+                             int64_t count, uint64_t* cw, int8_t* nerr, int sm_count, cudaStream_t st) {
     if (count <= 0) return cudaSuccess;
     const int sms = sm_count > 0 ? sm_count : 148;
     if (algo == 1) {
@@ -164,9 +170,14 @@ cudaError_t launch_rs_packed(const RsTables* tab, int t, int algo, const uint64_
             int64_t blocks = (groups + 255) / 256;
             const int64_t cap = static_cast<int64_t>(sms) * 16;
             if (blocks > cap) blocks = cap;
-            rs_t1_packed_x4_kernel<<<static_cast<unsigned>(blocks), 256, 0, st>>>(
-                tab, reinterpret_cast<const ulonglong2*>(words), groups, reinterpret_cast<ulonglong2*>(cw),
-                reinterpret_cast<uint32_t*>(nerr));
+            const auto* wv = reinterpret_cast<const ulonglong2*>(words);
+            auto* cv = reinterpret_cast<ulonglong2*>(cw);
+            auto* nv = reinterpret_cast<uint32_t*>(nerr);
+            const unsigned gb = static_cast<unsigned>(blocks);
+            if (m == 4 && r == 3) rs_t1_packed_x4_kernel<4, 3><<<gb, 256, 0, st>>>(tab, wv, groups, cv, nv);
+            else if (m == 4) rs_t1_packed_x4_kernel<4, 2><<<gb, 256, 0, st>>>(tab, wv, groups, cv, nv);
+            else if (r == 3) rs_t1_packed_x4_kernel<8, 3><<<gb, 256, 0, st>>>(tab, wv, groups, cv, nv);
+            else rs_t1_packed_x4_kernel<8, 2><<<gb, 256, 0, st>>>(tab, wv, groups, cv, nv);
         }
         const int64_t done = groups * 4, rest = count - done;
         if (rest > 0) {

@@ -4,7 +4,7 @@ Parity here is NOT pinned by the reference (it has no conv extractor,
 SPEC.md:364): the C oracle is cross-checked against a plain PyTorch fp32
 model built from the same parameters, and the sm_100a bf16 tensor-core path
 against the oracle with a stated tolerance:
-  * logits: relative L2 error <= 3e-2 (bf16 weights/activations, fp32 accumulate)
+  * logits: relative L2 error <= 1e-2 (bf16 weights/activations, tf32 first layer, fp32 accumulate)
   * hard bits: equal wherever |logit_ref| > 0.1 * rms(logit_ref)
   * RS-corrected messages / verify: bit-exact given the GPU's own hard bits.
 """
@@ -15,7 +15,7 @@ import oracle
 
 SEED = 7
 NB = 60
-REL_L2_TOL = 3e-2
+REL_L2_TOL = 1e-2
 NEAR_ZERO = 0.1
 
 
