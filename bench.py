@@ -327,6 +327,7 @@ def main():
                     "achieved_gbs": 17 * args.rs_words / (rms / 1e3) / 1e9}
     small = ne_true <= code.t
     assert bool((ne[small] == ne_true[small]).all())
+    cpu_words = words[:1_000_000].cpu().numpy().view(np.uint64)  # CPU-reference RS sample
     del words, cw, ne, msg
 
     # Learned extractor (SURVEY 8(d) "learned path"): 9 x conv3x3 64ch on
@@ -344,8 +345,7 @@ def main():
             cpu = {"value": statistics.median(rates), "unit": "images/s", "cores": info["cores"],
                    "kind": info["kind"], "sample": info["sample"]}
             nthreads = os.cpu_count() or 1
-            rs["cpu_reference_codewords_per_s"] = cpu_rs_baseline(
-                words[:1_000_000].cpu().numpy().view(np.uint64), nthreads)
+            rs["cpu_reference_codewords_per_s"] = cpu_rs_baseline(cpu_words, nthreads)
             rs["cpu_reference_sample"] = f"1,000,000 stress words, bw_decode on {nthreads} threads"
         except Exception as exc:  # the reference library may be absent
             cpu = {"value": None, "unit": "images/s", "cores": os.cpu_count(), "kind": "reference",

@@ -295,8 +295,10 @@ __global__ void __launch_bounds__(kC0Threads) conv0_kernel(const __grid_constant
         float x[kC0K];
 #pragma unroll
         for (int t = 0; t < 9; ++t) {
-            const int sx = px + t % 3 - 1;
-            const bool in = sx >= 0 && sx < kHSide;
+            // zero padding is in the normalised domain: taps outside the tile
+            // (either axis) contribute 0.0, not lut[0] = -1
+            const int sx = px + t % 3 - 1, sy = y0 + ry + t / 3 - 2;
+            const bool in = sx >= 0 && sx < kHSide && sy >= 0 && sy < kHSide;
             const uint8_t* rp = rows[ry + t / 3 - 1];
 #pragma unroll
             for (int c = 0; c < 3; ++c) x[t * 3 + c] = in ? lut[rp[sx * 3 + c]] : 0.0f;
