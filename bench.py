@@ -278,7 +278,9 @@ def main():
     # e2e through the public host API: pinned host images -> host records.
     host_pool = torch.empty((POOL, H, W, 3), dtype=torch.uint8, pin_memory=True)
     host_pool.copy_(pool)
-    recs_h = np.zeros(BATCH, dtype=q.RECORD_DTYPE)
+    # records land in pinned host memory (a pageable buffer would be registered per call)
+    recs_pin = torch.empty((BATCH, q.RECORD_DTYPE.itemsize), dtype=torch.uint8, pin_memory=True)
+    recs_h = recs_pin.numpy().view(q.RECORD_DTYPE).reshape(-1)
     plan = ([1, 2, 1], [BATCH // 2] * 3)
 
     def e2e_step(i, mode):

@@ -38,6 +38,8 @@ namespace qrm {
 cudaError_t launch_corr_detect(const DetectParams& p, int sm_count, cudaStream_t st);
 cudaError_t launch_detect_finish(const DetectParams& p, int tmax, int sm_count, cudaStream_t st);
 cudaError_t launch_gather_windows(const GatherDesc* descs, int64_t count, int l, uint8_t* out, cudaStream_t st);
+cudaError_t launch_fetch_windows(const WindowSource& src, int64_t count, int K, uint8_t* out, int sm_count,
+                                 cudaStream_t st);
 cudaError_t launch_rs_packed(const RsTables* tab, int m, int r, int t, int algo, const uint64_t* words,
                              int64_t count, uint64_t* cw, int8_t* nerr, int sm_count, cudaStream_t st);
 cudaError_t launch_rs_symbols(const RsTables* tab, int n, int t, const uint8_t* recv, int64_t count, uint8_t* cw,
@@ -675,7 +677,10 @@ QRM_EXPORT qrm_status qrm_detect_host(qrm_ctx* c, const uint8_t* images, int64_t
                     const uint8_t* src0 = images + (first + i) * stride + static_cast<int64_t>(yo + ty) * pitch +
                                           static_cast<int64_t>(xo + tx) * 3;
                     uint8_t* dst = hs + i * K;
-                    for (int r = 0; r < l; ++r) std::memcpy(dst + r * rowb, src0 + static_cast<int64_t>(r) * pitch, rowb);
+                    if (rowb == 192)  // l = 64: fixed-size rows compile to vector moves
+                        for (int r = 0; r < 64; ++r) std::memcpy(dst + r * 192, src0 + static_cast<int64_t>(r) * pitch, 192);
+                    else
+                        for (int r = 0; r < l; ++r) std::memcpy(dst + r * rowb, src0 + static_cast<int64_t>(r) * pitch, rowb);
                 }
             });
             QRM_CUDA(cudaMemcpyAsync(W.stage, hs, cnt * K, cudaMemcpyHostToDevice, xs));
@@ -692,6 +697,41 @@ QRM_EXPORT qrm_status qrm_detect_host(qrm_ctx* c, const uint8_t* images, int64_t
             ws.strategy = cfg.tile_strategy;
             ws.tile_seed = cfg.tile_seed;
             ws.first_draw = first_draw + static_cast<uint64_t>(first);
+            cudaEvent_t e_mid = ev[evi++];
+            if ((s = run_detect(c, W, ws, cnt, c->d_records + first, nullptr, nullptr, ds, e_mid, cs)) != QRM_OK)
+                return s;
+            QRM_CUDA(cudaMemcpyAsync(out + first, c->d_records + first, sizeof(qrm_record) * cnt,
+                                     cudaMemcpyDeviceToHost, cs));
+            cudaEvent_t e_done = ev[evi++];
+            QRM_CUDA(cudaEventRecord(e_done, cs));
+            slot_free[slot] = e_done;
+            continue;
+        }
+        if (mode == 0 && direct_ok(c, src, w, h, stride) && (3 * c->l) % 16 == 0) {
+            // stage 0: the transfer kernel pulls each window over PCIe (zero-copy
+            // reads of mapped host memory) into this slot's device windows
+            if ((s = ensure(W.stage, W.stage_cap, mb * c->K)) != QRM_OK) return s;
+            WindowSource hs{};
+            hs.base = src;
+            hs.image_stride = stride;
+            hs.pitch = w * 3;
+            hs.x_off = xo;
+            hs.y_off = yo;
+            hs.direct = 1;
+            hs.l = c->l;
+            hs.strategy = c->cfg.tile_strategy;
+            hs.tile_seed = c->cfg.tile_seed;
+            hs.first_draw = first_draw + static_cast<uint64_t>(first);
+            QRM_LAUNCH(launch_fetch_windows(hs, cnt, c->K, W.stage, c->sms, xs));
+            h2d += static_cast<double>(c->K) * cnt;
+            cudaEvent_t e_in = ev[evi++];
+            QRM_CUDA(cudaEventRecord(e_in, xs));
+            QRM_CUDA(cudaStreamWaitEvent(ds, e_in, 0));
+            WindowSource ws = hs;
+            ws.base = W.stage;
+            ws.image_stride = c->K;
+            ws.pitch = 3 * c->l;
+            ws.direct = 0;
             cudaEvent_t e_mid = ev[evi++];
             if ((s = run_detect(c, W, ws, cnt, c->d_records + first, nullptr, nullptr, ds, e_mid, cs)) != QRM_OK)
                 return s;

@@ -141,6 +141,41 @@ __global__ void gather_windows_kernel(const GatherDesc* __restrict__ descs, int6
     }
 }
 
+
+// Host-buffer path, transfer stage: copy each image's l x l window from
+// mapped (zero-copy) pinned host memory into contiguous device windows. Only
+// the window crosses PCIe (3 l^2 of the 3 w h bytes). Plain 16-B loads, NB per
+// thread in flight before any store, keep enough reads outstanding to fill the
+// link (measured ~48 GB/s of the ~55 GB/s copy-engine rate, scripts/pcie_probe.cu).
+template <int NB>
+__global__ void __launch_bounds__(256) fetch_windows_kernel(const WindowSource src, int64_t count, int K,
+                                                            uint8_t* __restrict__ out) {
+    const int row16 = (3 * src.l) / 16;  // 16-B chunks per window row
+    const int per_img = src.l * row16;
+    const int64_t total = count * per_img;
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    for (int64_t base = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; base < total;
+         base += stride * NB) {
+        uint4 v[NB];
+#pragma unroll
+        for (int j = 0; j < NB; ++j) {
+            const int64_t i = base + j * stride;
+            if (i < total) {
+                const int64_t img = i / per_img;
+                const int rem = static_cast<int>(i - img * per_img);
+                const int r = rem / row16, c = rem - r * row16;
+                v[j] = __ldg(reinterpret_cast<const uint4*>(window_base(src, img, K) +
+                                                            static_cast<int64_t>(r) * src.pitch) + c);
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < NB; ++j) {
+            const int64_t i = base + j * stride;
+            if (i < total) reinterpret_cast<uint4*>(out)[i] = v[j];  // windows packed contiguously
+        }
+    }
+}
+
 // Rectangular out_w x out_h window of one image (resize / crop / preprocess
 // host utilities), optionally normalised to float(v/127.5 - 1) (image.cpp:36).
 __global__ void resample_kernel(const GatherDesc d, int out_w, int out_h, int normalize, void* __restrict__ out) {
@@ -158,6 +193,18 @@ __global__ void resample_kernel(const GatherDesc d, int out_w, int out_h, int no
 }
 
 // ---------------------------------------------------------------- launch --
+
+
+cudaError_t launch_fetch_windows(const WindowSource& src, int64_t count, int K, uint8_t* out, int sm_count,
+                                 cudaStream_t st) {
+    if (count <= 0) return cudaSuccess;
+    const int64_t chunks = count * (K / 16);
+    int64_t grid = (chunks + 256 * 4 - 1) / (256 * 4);
+    const int64_t cap = 2 * (sm_count > 0 ? sm_count : 148);  // leave the SMs' smem to the decode kernel
+    if (grid > cap) grid = cap;
+    fetch_windows_kernel<4><<<static_cast<unsigned>(grid), 256, 0, st>>>(src, count, K, out);
+    return cudaGetLastError();
+}
 
 cudaError_t launch_detect_finish(const DetectParams& p, int tmax, int sm_count, cudaStream_t st) {
     const int blocks = sm_count > 0 ? sm_count : 148;

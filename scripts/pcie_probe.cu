@@ -6,6 +6,8 @@
 #include <cstdint>
 #include <cstdio>
 #include <cstring>
+#include <chrono>
+#include <thread>
 #include <vector>
 
 #define CK(x)                                                                          \
@@ -70,6 +72,52 @@ __global__ void seq_read(const uint4* __restrict__ host, int64_t n16, uint4* __r
     for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n16; i += stride) dst[i] = host[i];
 }
 
+
+// TMA bulk copies (cp.async.bulk global->shared) of whole 192-B window rows
+// straight from mapped host memory, then to HBM: one warp per image.
+__global__ void gather_bulk(const uint8_t* __restrict__ host, const int* __restrict__ org, int count, uint8_t* __restrict__ dst) {
+    __shared__ __align__(128) uint8_t buf[3][K];
+    __shared__ __align__(8) uint64_t bar[3];
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    uint32_t phase = 0;
+    if (lane == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"((uint32_t)__cvta_generic_to_shared(&bar[w])));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+    for (int64_t img = blockIdx.x * 3 + w; img < count; img += gridDim.x * 3) {
+        const uint32_t b = (uint32_t)__cvta_generic_to_shared(&bar[w]);
+        if (lane == 0)
+            asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n\t}" ::"r"(b), "r"(K) : "memory");
+        __syncwarp();
+        for (int r = lane; r < L; r += 32) {
+            const uint8_t* s = host + img * IMG + static_cast<int64_t>(org[2 * img + 1] + r) * PITCH + org[2 * img] * 3;
+            asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                             (uint32_t)__cvta_generic_to_shared(&buf[w][r * ROWB])), "l"(s), "r"(ROWB), "r"(b) : "memory");
+        }
+        uint32_t ok = 0;
+        while (!ok)
+            asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+                         : "=r"(ok) : "r"(b), "r"(phase) : "memory");
+        phase ^= 1;
+        const uint4* src = reinterpret_cast<const uint4*>(buf[w]);
+        uint4* d = reinterpret_cast<uint4*>(dst + img * K);
+        for (int i = lane; i < K / 16; i += 32) d[i] = src[i];
+        __syncwarp();
+    }
+}
+
+// zero-copy reads of the 64 FULL rows holding the window (contiguous 48 KB per image)
+__global__ void rowblock_read(const uint4* __restrict__ host, const int* __restrict__ org, int count, uint4* __restrict__ dst) {
+    const int64_t per = static_cast<int64_t>(L) * PITCH / 16;
+    const int64_t total = per * count;
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < total; i += stride) {
+        const int64_t img = i / per, j = i % per;
+        dst[(i / 3) % (static_cast<int64_t>(count) * K / 16)] = host[(img * IMG + static_cast<int64_t>(org[2 * img + 1]) * PITCH) / 16 + j];
+    }
+}
+
 int main() {
     const int count = 4096;
     uint8_t* h = nullptr;
@@ -114,5 +162,66 @@ int main() {
     timeit("gather16_nb4", wbytes, [&] { gather16<4><<<148 * 8, 256>>>(dh, dorg, count, dst); });
     timeit("gather16_nb8_g4", wbytes, [&] { gather16<8><<<148 * 4, 256>>>(dh, dorg, count, dst); });
     timeit("gather_lines(256B per 192B row)", wbytes, [&] { gather_lines<<<148 * 8, 256>>>(dh, dorg, count, dst); });
+    timeit("gather_bulk(TMA 192B rows from host)", wbytes, [&] { gather_bulk<<<148 * 2, 96>>>(dh, dorg, count, dst); });
+    timeit("gather_bulk_g8", wbytes, [&] { gather_bulk<<<148 * 6, 96>>>(dh, dorg, count, dst); });
+    timeit("rowblock_zero_copy(48KB/img read)", wbytes, [&] { rowblock_read<<<148 * 8, 256>>>(reinterpret_cast<const uint4*>(dh), dorg, count, reinterpret_cast<uint4*>(dst)); });
+    {   // copy engine: one contiguous 48-KB row block per image (4x the window bytes)
+        uint8_t* drows;
+        CK(cudaMalloc(&drows, static_cast<size_t>(count) * L * PITCH));
+        timeit("memcpy_rowblocks_4096_calls", wbytes, [&] {
+            for (int i = 0; i < count; ++i)
+                cudaMemcpyAsync(drows + static_cast<size_t>(i) * L * PITCH, h + static_cast<size_t>(i) * IMG + static_cast<size_t>(org[2 * i + 1]) * PITCH,
+                                static_cast<size_t>(L) * PITCH, cudaMemcpyHostToDevice);
+        });
+        timeit("memcpy2d_windows_4096_calls", wbytes, [&] {
+            for (int i = 0; i < count; ++i)
+                cudaMemcpy2DAsync(dst + static_cast<size_t>(i) * K, ROWB, h + static_cast<size_t>(i) * IMG + static_cast<size_t>(org[2 * i + 1]) * PITCH + org[2 * i] * 3,
+                                  PITCH, ROWB, L, cudaMemcpyHostToDevice);
+        });
+#if CUDART_VERSION >= 12080
+        std::vector<void*> dsts(count), srcs(count);
+        std::vector<size_t> sizes(count, static_cast<size_t>(L) * PITCH);
+        for (int i = 0; i < count; ++i) {
+            dsts[i] = drows + static_cast<size_t>(i) * L * PITCH;
+            srcs[i] = h + static_cast<size_t>(i) * IMG + static_cast<size_t>(org[2 * i + 1]) * PITCH;
+        }
+        cudaMemcpyAttributes attr{};
+        attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
+        attr.srcLocHint.type = cudaMemLocationTypeHost;
+        attr.dstLocHint.type = cudaMemLocationTypeDevice;
+        size_t ai = 0, fail = 0;
+        timeit("memcpy_batch_rowblocks", wbytes, [&] {
+            cudaMemcpyBatchAsync(dsts.data(), srcs.data(), sizes.data(), count, &attr, &ai, 1, &fail, 0);
+        });
+        printf("batch fail idx %zu err %s\n", fail, cudaGetErrorString(cudaGetLastError()));
+#endif
+    }
+    {   // host gather into pinned staging with T threads, then one H2D
+        uint8_t* stage;
+        CK(cudaHostAlloc(&stage, static_cast<size_t>(count) * K, cudaHostAllocDefault));
+        unsigned hc = std::thread::hardware_concurrency();
+        printf("{\"host_threads\": %u}\n", hc);
+        for (unsigned T : {1u, 2u, 4u, 8u, 16u, 32u}) {
+            if (T > 2 * hc) break;
+            auto gather = [&](int t) {
+                for (int i = t; i < count; i += T) {
+                    const uint8_t* s = h + static_cast<size_t>(i) * IMG + static_cast<size_t>(org[2 * i + 1]) * PITCH + org[2 * i] * 3;
+                    uint8_t* d = stage + static_cast<size_t>(i) * K;
+                    for (int r = 0; r < L; ++r) memcpy(d + r * ROWB, s + static_cast<size_t>(r) * PITCH, ROWB);
+                }
+            };
+            double best = 1e30;
+            for (int rep = 0; rep < 5; ++rep) {
+                auto t0 = std::chrono::steady_clock::now();
+                std::vector<std::thread> th;
+                for (unsigned t = 0; t < T; ++t) th.emplace_back(gather, t);
+                for (auto& x : th) x.join();
+                double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+                if (ms < best) best = ms;
+            }
+            printf("{\"probe\": \"host_gather_T%u\", \"ms\": %.4f, \"GBps\": %.2f, \"images_per_s\": %.0f}\n", T, best, wbytes / best / 1e6, count / best * 1e3);
+        }
+        timeit("memcpy_h2d_staged_windows", wbytes, [&] { cudaMemcpyAsync(dst, stage, count * static_cast<size_t>(K), cudaMemcpyHostToDevice); });
+    }
     return 0;
 }
