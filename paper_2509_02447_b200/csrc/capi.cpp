@@ -993,7 +993,7 @@ QRM_EXPORT qrm_status qrm_hidden_detect_device(qrm_ctx* c, const uint8_t* images
     if ((s = window_source(c, W, images, count, w, h, stride, first_draw, st, src)) != QRM_OK) return s;
     auto& H = c->hid;
     Conv0Params p0{src, count, c->K, H.w0, H.bias, H.act[0]};
-    QRM_LAUNCH(launch_conv0(p0, H.tmap_st[0], st));
+    QRM_LAUNCH(launch_conv0(p0, H.tmap_st[0], c->sms, st));
     for (int j = 1; j < kHiddenLayers; ++j) {
         HiddenLayerParams lp{};
         lp.w_swizzled = H.w_sw + static_cast<int64_t>(j - 1) * 9 * 64 * 64;
@@ -1043,7 +1043,7 @@ QRM_EXPORT qrm_status qrm_hidden_debug_activation(qrm_ctx* c, const uint8_t* ima
     if ((s = window_source(c, W, images, count, w, h, stride, first_draw, st, src)) != QRM_OK) return s;
     auto& H = c->hid;
     Conv0Params p0{src, count, c->K, H.w0, H.bias, H.act[0]};
-    QRM_LAUNCH(launch_conv0(p0, H.tmap_st[0], st));
+    QRM_LAUNCH(launch_conv0(p0, H.tmap_st[0], c->sms, st));
     for (int j = 1; j <= stop_after; ++j) {
         HiddenLayerParams lp{};
         lp.w_swizzled = H.w_sw + static_cast<int64_t>(j - 1) * 9 * 64 * 64;

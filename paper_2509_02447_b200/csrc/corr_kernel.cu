@@ -180,9 +180,11 @@ __global__ void __launch_bounds__(kCorrThreads, 1) corr_detect_kernel(const __gr
             const uint32_t b_s = a_s + kCorrABytes;
             if (kbyte < p.K) {
                 const int64_t off = static_cast<int64_t>(trow) * pitch + tcol;
+                // .L2::64B: fill only the 64-B sector pairs the 192-B row covers (the
+                // default 128-B fill over-reads 1.33x: ncu 68.0 -> 51.2 MB per 50.3 MB)
 #pragma unroll
                 for (int j = 0; j < 8; ++j)
-                    if (valid[j]) cp_async16(a_s + sw128_offset(rb + 16 * j, c), wb[j] + off);
+                    if (valid[j]) cp_async16_l2_64(a_s + sw128_offset(rb + 16 * j, c), wb[j] + off);
             }
 #pragma unroll
             for (int j = 0; j < 4; ++j) {

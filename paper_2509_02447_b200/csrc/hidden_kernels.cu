@@ -49,7 +49,6 @@ struct HiddenSmem {
     uint64_t a_full[kHAStages], a_empty[kHAStages];
     uint64_t acc_full[2], acc_empty[2];
     uint32_t tmem_base;
-    float bias[kHC];
     float pool[4][kHC];  // per-epilogue-warp channel sums (last layer)
 };
 constexpr int kHOBytes = 4 * 32 * kHC * 2;  // 16 KB: output staging, 4 KB per epilogue warp
@@ -62,6 +61,7 @@ __global__ void __launch_bounds__(kHThreads, 1)
     conv64_kernel(const __grid_constant__ CUtensorMap tmap_in, const __grid_constant__ CUtensorMap tmap_out,
                   const __grid_constant__ HiddenLayerParams p) {
     extern __shared__ uint8_t smem_raw[];
+    __shared__ float s_bias[kHC];  // static: read with LDS broadcasts in the epilogue
     uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const uint32_t w_s = smem_u32(base);
     const uint32_t a_s0 = w_s + kHWBytes;
@@ -84,7 +84,7 @@ __global__ void __launch_bounds__(kHThreads, 1)
         }
         mbar_fence_init();
     }
-    if (tid < kHC) sm.bias[tid] = p.bias[tid];
+    if (tid < kHC) s_bias[tid] = p.bias[tid];
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -169,7 +169,7 @@ __global__ void __launch_bounds__(kHThreads, 1)
             const int pix = static_cast<int>(b % kHBlocks) * kHM + q * 32 + lane;
             float v[kHC];
 #pragma unroll
-            for (int c = 0; c < kHC; ++c) v[c] = fmaxf(__uint_as_float(acc[c]) + sm.bias[c], 0.0f);
+            for (int c = 0; c < kHC; ++c) v[c] = fmaxf(__uint_as_float(acc[c]) + s_bias[c], 0.0f);
             if (!p.last) {
                 // Stage this warp's 32 pixels x 128 B as a 128B-swizzled slab (16-B
                 // chunk c of row r at chunk c ^ (r & 7): conflict free), then one TMA
@@ -236,28 +236,28 @@ __global__ void __launch_bounds__(kHThreads, 1)
 // First layer (3 -> 64, K = 27) as one tcgen05 kind::tf32 GEMM per 128-pixel
 // block: D[128 px][64 co] = A[128 px][32] . W0[64 co][32]^T, K = 27 taps x
 // channels zero-padded to 32 (fp32 rows of exactly 128 B, one 128B-swizzle
-// atom row). The CTA stages the block's 4 input rows (u8) in shared memory,
-// each thread builds its pixel's im2col row from a 256-entry normalisation
-// table (float(v/127.5 - 1), image.cpp:36, rounded to tf32) and one thread
-// issues the 4 MMAs (K = 8 each). Epilogue as conv64: bias + ReLU -> bf16 rows
-// 128B-swizzled into a per-warp staging slab -> one TMA store per warp. Small
-// CTAs (24 KB smem, 64 TMEM columns) so several blocks overlap per SM.
+// atom row). Persistent CTAs (several per SM) set up once — normalisation
+// table (float(v/127.5 - 1), image.cpp:36, rounded to tf32), folded weights,
+// TMEM — then loop over blocks: stage the block's 4 input rows (u8), build
+// each pixel's im2col row, one thread issues the 4 MMAs (K = 8 each), and the
+// epilogue (bias + ReLU -> bf16, 128B-swizzled per-warp slab, one TMA store per
+// warp) drains TMEM. The A tile doubles as the output staging slab.
 constexpr int kC0Threads = 128;
 constexpr int kC0K = 32;  // padded K (fp32 elements per A/B row)
 
 __global__ void __launch_bounds__(kC0Threads) conv0_kernel(const __grid_constant__ CUtensorMap tmap_out,
                                                            const __grid_constant__ Conv0Params p) {
-    __shared__ __align__(1024) uint8_t a_tile[kHM * kC0K * 4];  // 16 KB A (reused as output staging)
+    __shared__ __align__(1024) uint8_t a_tile[kHM * kC0K * 4];  // 16 KB A (im2col, fp32/tf32)
+    __shared__ __align__(1024) uint8_t o_tile[kHM * kHC * 2];   // 16 KB output staging (4 KB per warp)
     __shared__ __align__(1024) uint8_t b_tile[kHC * kC0K * 4];  // 8 KB W0 (pre-swizzled)
     __shared__ float lut[256];
     __shared__ float bsh[kHC];
-    __shared__ uint8_t rows[4][3 * kHSide];
+    __shared__ __align__(16) uint8_t rows[4][3 * kHSide];
     __shared__ uint64_t done;
     __shared__ uint32_t tmem_slot;
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int64_t tile = blockIdx.x / kHBlocks;
-    const int blk = static_cast<int>(blockIdx.x % kHBlocks);
+    const int64_t nblocks = p.tiles * kHBlocks;
     if (warp == 0) tmem_alloc<kHC>(&tmem_slot);
     if (tid == 0) {
         mbar_init(&done, 1);
@@ -278,85 +278,106 @@ __global__ void __launch_bounds__(kC0Threads) conv0_kernel(const __grid_constant
         for (int i = 0; i < (kHC * kC0K * 4) / 16 / kC0Threads; ++i)
             dst[tid + i * kC0Threads] = __ldg(src + tid + i * kC0Threads);
     }
-    // the 4 input rows y0-1 .. y0+2 (zero outside the tile)
-    const uint8_t* wb = window_base(p.src, tile, p.K);
-    const int pitch = p.src.direct ? p.src.pitch : 3 * kHSide;
-    const int y0 = blk * 2;
-    for (int i = tid; i < 4 * 3 * kHSide; i += kC0Threads) {
-        const int r = i / (3 * kHSide), x = i - r * (3 * kHSide);
-        const int sy = y0 - 1 + r;
-        rows[r][x] = (sy >= 0 && sy < kHSide) ? wb[static_cast<int64_t>(sy) * pitch + x] : uint8_t{0};
-    }
-    __syncthreads();
-
-    // im2col row of pixel (y0 + tid/64, tid%64): k = tap*3 + c, tap = 3(dy+1) + (dx+1)
-    {
-        const int ry = 1 + (tid >> 6), px = tid & 63;
-        float x[kC0K];
-#pragma unroll
-        for (int t = 0; t < 9; ++t) {
-            // zero padding is in the normalised domain: taps outside the tile
-            // (either axis) contribute 0.0, not lut[0] = -1
-            const int sx = px + t % 3 - 1, sy = y0 + ry + t / 3 - 2;
-            const bool in = sx >= 0 && sx < kHSide && sy >= 0 && sy < kHSide;
-            const uint8_t* rp = rows[ry + t / 3 - 1];
-#pragma unroll
-            for (int c = 0; c < 3; ++c) x[t * 3 + c] = in ? lut[rp[sx * 3 + c]] : 0.0f;
-        }
-#pragma unroll
-        for (int k = 27; k < kC0K; ++k) x[k] = 0.0f;
-        const uint32_t row = smem_u32(a_tile) + tid * 128;
-#pragma unroll
-        for (int c = 0; c < 8; ++c)
-            st_shared_v4(row + (((c ^ tid) & 7) << 4),
-                         make_uint4(__float_as_uint(x[4 * c]), __float_as_uint(x[4 * c + 1]),
-                                    __float_as_uint(x[4 * c + 2]), __float_as_uint(x[4 * c + 3])));
-    }
-    fence_proxy_async_smem();  // generic-proxy writes of A and B -> visible to the tensor core
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = tmem_slot;
-    if (tid == 0) {
-        const uint32_t idesc = idesc_tf32_f32(kHM, kHC);
-        const uint64_t da = sw128_kmajor_desc(smem_u32(a_tile)), db = sw128_kmajor_desc(smem_u32(b_tile));
+    const uint32_t idesc = idesc_tf32_f32(kHM, kHC);
+    const uint64_t da = sw128_kmajor_desc(smem_u32(a_tile)), db = sw128_kmajor_desc(smem_u32(b_tile));
+    const int pitch = p.src.direct ? p.src.pitch : 3 * kHSide;
+    constexpr int kRow16 = 3 * kHSide / 16;  // 12 16-B chunks per input row; threads < 48 move one each
+
+    // Software pipeline: the 4 input rows of block b+grid are fetched into
+    // registers while block b is computed, so the DRAM latency overlaps.
+    auto fetch = [&](int64_t b, uint4& v) -> bool {
+        if (tid >= 4 * kRow16 || b >= nblocks) return false;
+        const int64_t tile = b / kHBlocks;
+        const int sy = static_cast<int>(b % kHBlocks) * 2 - 1 + tid / kRow16;
+        if (sy < 0 || sy >= kHSide) return false;  // zero-padded by the im2col below
+        v = __ldg(reinterpret_cast<const uint4*>(window_base(p.src, tile, p.K) + static_cast<int64_t>(sy) * pitch) +
+                  tid % kRow16);
+        return true;
+    };
+    uint4 pre = make_uint4(0, 0, 0, 0);
+    bool have = fetch(blockIdx.x, pre);
+    uint32_t phase = 0;
+
+    for (int64_t b = blockIdx.x; b < nblocks; b += gridDim.x, phase ^= 1) {
+        const int64_t tile = b / kHBlocks;
+        const int blk = static_cast<int>(b % kHBlocks);
+        const int y0 = blk * 2;
+        if (have) reinterpret_cast<uint4*>(rows[tid / kRow16])[tid % kRow16] = pre;
+        __syncthreads();
+        have = fetch(b + gridDim.x, pre);
+
+        // im2col row of pixel (y0 + tid/64, tid%64): k = tap*3 + c, tap = 3(dy+1) + (dx+1)
+        {
+            const int ry = 1 + (tid >> 6), px = tid & 63;
+            float x[kC0K];
 #pragma unroll
-        for (int k = 0; k < kC0K / 8; ++k) umma_tf32(tmem, da + 2 * k, db + 2 * k, idesc, k != 0);
-        umma_commit(&done);
+            for (int t = 0; t < 9; ++t) {
+                // zero padding is in the normalised domain: taps outside the tile
+                // (either axis) contribute 0.0, not lut[0] = -1
+                const int sx = px + t % 3 - 1, sy = y0 + ry + t / 3 - 2;
+                const bool in = sx >= 0 && sx < kHSide && sy >= 0 && sy < kHSide;
+                const uint8_t* rp = rows[ry + t / 3 - 1];
+#pragma unroll
+                for (int c = 0; c < 3; ++c) x[t * 3 + c] = in ? lut[rp[sx * 3 + c]] : 0.0f;
+            }
+#pragma unroll
+            for (int k = 27; k < kC0K; ++k) x[k] = 0.0f;
+            const uint32_t row = smem_u32(a_tile) + tid * 128;
+#pragma unroll
+            for (int c = 0; c < 8; ++c)
+                st_shared_v4(row + (((c ^ tid) & 7) << 4),
+                             make_uint4(__float_as_uint(x[4 * c]), __float_as_uint(x[4 * c + 1]),
+                                        __float_as_uint(x[4 * c + 2]), __float_as_uint(x[4 * c + 3])));
+        }
+        fence_proxy_async_smem();  // generic-proxy writes of A -> visible to the tensor core
+        tc_fence_before();
+        __syncthreads();
+        tc_fence_after();
+        if (tid == 0) {
+#pragma unroll
+            for (int k = 0; k < kC0K / 8; ++k) umma_tf32(tmem, da + 2 * k, db + 2 * k, idesc, k != 0);
+            umma_commit(&done);
+        }
+        mbar_wait(&done, phase);
+        tc_fence_after();
+        uint32_t acc[kHC];
+#pragma unroll
+        for (int c = 0; c < kHC / 16; ++c) {
+            uint32_t r16[16];
+            tmem_ld16(tmem + (static_cast<uint32_t>(warp * 32) << 16) + c * 16, r16);
+#pragma unroll
+            for (int j = 0; j < 16; ++j) acc[c * 16 + j] = r16[j];
+        }
+        tmem_ld_wait();
+        tc_fence_before();
+        // this warp's previous output store must have read its slab (issued a block ago)
+        if (lane == 0) bulk_wait_read<0>();
+        __syncwarp();
+        const uint32_t slab = smem_u32(o_tile) + warp * 4096;
+        const uint32_t row = slab + lane * 128;
+#pragma unroll
+        for (int c = 0; c < kHC; c += 8) {
+            float v[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) v[j] = fmaxf(__uint_as_float(acc[c + j]) + bsh[c + j], 0.0f);
+            __nv_bfloat162 h0 = __floats2bfloat162_rn(v[0], v[1]), h1 = __floats2bfloat162_rn(v[2], v[3]);
+            __nv_bfloat162 h2 = __floats2bfloat162_rn(v[4], v[5]), h3 = __floats2bfloat162_rn(v[6], v[7]);
+            st_shared_v4(row + ((((c >> 3) ^ lane) & 7) << 4),
+                         make_uint4(*reinterpret_cast<uint32_t*>(&h0), *reinterpret_cast<uint32_t*>(&h1),
+                                    *reinterpret_cast<uint32_t*>(&h2), *reinterpret_cast<uint32_t*>(&h3)));
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+            tma_store_2d(&tmap_out, slab, 0, static_cast<int>(tile * kHPix + blk * kHM + warp * 32));
+            bulk_commit();
+        }
     }
-    mbar_wait(&done, 0);
-    tc_fence_after();
-    uint32_t acc[kHC];
-#pragma unroll
-    for (int c = 0; c < kHC / 16; ++c) {
-        uint32_t r16[16];
-        tmem_ld16(tmem + (static_cast<uint32_t>(warp * 32) << 16) + c * 16, r16);
-#pragma unroll
-        for (int j = 0; j < 16; ++j) acc[c * 16 + j] = r16[j];
-    }
-    tmem_ld_wait();
-    // the MMAs completed (done), so A is free: stage the bf16 output rows in it
-    const uint32_t slab = smem_u32(a_tile) + warp * 4096;
-    const uint32_t row = slab + lane * 128;
-#pragma unroll
-    for (int c = 0; c < kHC; c += 8) {
-        float v[8];
-#pragma unroll
-        for (int j = 0; j < 8; ++j) v[j] = fmaxf(__uint_as_float(acc[c + j]) + bsh[c + j], 0.0f);
-        __nv_bfloat162 h0 = __floats2bfloat162_rn(v[0], v[1]), h1 = __floats2bfloat162_rn(v[2], v[3]);
-        __nv_bfloat162 h2 = __floats2bfloat162_rn(v[4], v[5]), h3 = __floats2bfloat162_rn(v[6], v[7]);
-        st_shared_v4(row + ((((c >> 3) ^ lane) & 7) << 4),
-                     make_uint4(*reinterpret_cast<uint32_t*>(&h0), *reinterpret_cast<uint32_t*>(&h1),
-                                *reinterpret_cast<uint32_t*>(&h2), *reinterpret_cast<uint32_t*>(&h3)));
-    }
-    fence_proxy_async_smem();
-    __syncwarp();
-    if (lane == 0) {
-        tma_store_2d(&tmap_out, slab, 0, static_cast<int>(tile * kHPix + blk * kHM + warp * 32));
-        bulk_commit();
-        bulk_wait_read<0>();  // the slab must stay valid until the store has read it
-    }
-    tc_fence_before();
+    if (lane == 0) bulk_wait<0>();
     __syncthreads();
     if (warp == 0) {
         tc_fence_after();
@@ -486,8 +507,10 @@ cudaError_t launch_hidden_prep(uint64_t seed, int nbits, __nv_bfloat16* w_sw, fl
     return cudaGetLastError();
 }
 
-cudaError_t launch_conv0(const Conv0Params& p, const CUtensorMap& tmap_out, cudaStream_t st) {
-    conv0_kernel<<<static_cast<unsigned>(p.tiles * kHBlocks), kC0Threads, 0, st>>>(tmap_out, p);
+cudaError_t launch_conv0(const Conv0Params& p, const CUtensorMap& tmap_out, int sm_count, cudaStream_t st) {
+    int64_t grid = static_cast<int64_t>(sm_count > 0 ? sm_count : 148) * 4;  // 4 resident per SM (118 regs x 128 thr)
+    if (grid > p.tiles * kHBlocks) grid = p.tiles * kHBlocks;
+    conv0_kernel<<<static_cast<unsigned>(grid), kC0Threads, 0, st>>>(tmap_out, p);
     return cudaGetLastError();
 }
 

@@ -106,6 +106,13 @@ QRM_D void cp_async16(uint32_t dst_smem, const void* src, uint32_t src_bytes = 1
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst_smem), "l"(src), "r"(src_bytes)
                  : "memory");
 }
+// As cp_async16 with an explicit L2 fill-size hint (64 / 128 / 256 B).
+QRM_D void cp_async16_l2_64(uint32_t dst_smem, const void* src) {
+    asm volatile("cp.async.cg.shared.global.L2::64B [%0], [%1], 16;" ::"r"(dst_smem), "l"(src) : "memory");
+}
+QRM_D void cp_async16_l2_256(uint32_t dst_smem, const void* src) {
+    asm volatile("cp.async.cg.shared.global.L2::256B [%0], [%1], 16;" ::"r"(dst_smem), "l"(src) : "memory");
+}
 QRM_D void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
 QRM_D void cp_async_wait() {

@@ -48,7 +48,7 @@ struct HeadParams {
 
 cudaError_t launch_hidden_prep(uint64_t seed, int nbits, __nv_bfloat16* w_sw, float* bias, float* w0, float* wl,
                                float* bl, cudaStream_t st);
-cudaError_t launch_conv0(const Conv0Params& p, const CUtensorMap& tmap_out, cudaStream_t st);
+cudaError_t launch_conv0(const Conv0Params& p, const CUtensorMap& tmap_out, int sm_count, cudaStream_t st);
 // tmap: 4-D load map of the input activations; tmap_out: 2-D store map of the
 // output activations ({64 ch, T*4096 px}, box {64, 32}, 128B swizzle).
 cudaError_t launch_conv64(const CUtensorMap& tmap, const CUtensorMap& tmap_out, const HiddenLayerParams& p,
