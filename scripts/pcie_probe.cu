@@ -223,5 +223,30 @@ int main() {
         }
         timeit("memcpy_h2d_staged_windows", wbytes, [&] { cudaMemcpyAsync(dst, stage, count * static_cast<size_t>(K), cudaMemcpyHostToDevice); });
     }
+    {   // device-resident images: how fast can the window gather pattern stream from HBM?
+        const int dcount = 16384;
+        uint8_t *dpool, *dwin;
+        int* dorg2;
+        CK(cudaMalloc(&dpool, static_cast<size_t>(dcount) * IMG));
+        CK(cudaMemset(dpool, 1, static_cast<size_t>(dcount) * IMG));
+        CK(cudaMalloc(&dwin, static_cast<size_t>(dcount) * K));
+        std::vector<int> org2(2 * dcount);
+        for (int i = 0; i < dcount; ++i) {
+            org2[2 * i] = ((i * 7) % 4) * 64;
+            org2[2 * i + 1] = ((i * 13) % 4) * 64;
+        }
+        CK(cudaMalloc(&dorg2, sizeof(int) * 2 * dcount));
+        CK(cudaMemcpy(dorg2, org2.data(), sizeof(int) * 2 * dcount, cudaMemcpyHostToDevice));
+        for (int n : {4096, 16384}) {
+            const double wb = static_cast<double>(n) * K;
+            char name[64];
+            snprintf(name, sizeof name, "hbm_gather16_nb4_%d", n);
+            timeit(name, wb, [&] { gather16<4><<<148 * 8, 256>>>(dpool, dorg2, n, dwin); });
+            snprintf(name, sizeof name, "hbm_gather_lines_%d", n);
+            timeit(name, wb, [&] { gather_lines<<<148 * 8, 256>>>(dpool, dorg2, n, dwin); });
+            snprintf(name, sizeof name, "hbm_seq_copy_%d", n);
+            timeit(name, wb, [&] { seq_read<<<148 * 8, 256>>>(reinterpret_cast<const uint4*>(dpool) + (n * static_cast<int64_t>(K) / 16), n * static_cast<int64_t>(K) / 16, reinterpret_cast<uint4*>(dwin)); });
+        }
+    }
     return 0;
 }
