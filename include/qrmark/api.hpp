@@ -322,6 +322,12 @@ struct CacheConfig {
     size_t capacity = 4096;
     uint64_t stale_after = 1u << 20;
 };
+// Extractor behind the WatermarkCodec plug-in point (stego.hpp:32-40). Additive
+// to the reference config (whose DetectionContext holds a SpreadSpectrumCodec,
+// detect.hpp:106-114): `conv` selects the learned HiDDeN-style conv stack
+// (tcgen05 bf16; contract oracle/hidden_oracle.c) with random-init weights
+// drawn from conv_weight_seed. RS correction / verify are unchanged.
+enum class ExtractorKind { spread_spectrum, conv };
 struct DetectionConfig {
     CodeParams code;
     TileSpec tile;
@@ -330,6 +336,8 @@ struct DetectionConfig {
     int rs_workers = 32;
     double fpr_target = 1e-6;
     CacheConfig cache;
+    ExtractorKind extractor = ExtractorKind::spread_spectrum;
+    uint64_t conv_weight_seed = 7;
     static DetectionConfig make(const CodeParams& code, const TileSpec& tile, uint64_t key_seed, double alpha,
                                 BitVec key_message);
 };

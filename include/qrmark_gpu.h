@@ -159,6 +159,17 @@ QRM_EXPORT qrm_status qrm_hidden_detect_device(qrm_ctx* ctx, const uint8_t* imag
                                                int64_t image_stride, uint64_t first_draw, uint64_t weight_seed,
                                                float* logits, qrm_record* out, void* stream);
 
+/* Extractor behind the WatermarkCodec plug-in point (stego.hpp:32-40) used by
+ * qrm_detect_device / qrm_detect_host / qrm_detect_ragged:
+ *   QRM_EXTRACTOR_SPREAD_SPECTRUM (default): SpreadSpectrumCodec::extract
+ *     (stego.cpp:53-67), the reference's own extractor;
+ *   QRM_EXTRACTOR_CONV: the learned conv stack of qrm_hidden_detect_device
+ *     with weights drawn from weight_seed (needs tile_size 64).
+ * RS correction, verify and the record layout are the same for both. */
+#define QRM_EXTRACTOR_SPREAD_SPECTRUM 0
+#define QRM_EXTRACTOR_CONV 1
+QRM_EXPORT qrm_status qrm_ctx_set_extractor(qrm_ctx* ctx, int kind, uint64_t weight_seed);
+
 /* preprocess (transforms.cpp:42-47) of one host image -> 256*256*3 floats. */
 QRM_EXPORT qrm_status qrm_preprocess_host(const uint8_t* image, int w, int h, float* out);
 

@@ -27,6 +27,7 @@ LIB_PATH = os.path.join(_HERE, "_lib", "libqrmark_b200.so")
 # Exported symbols of include/qrmark_gpu.h (checked by the CPU test suite).
 ABI_SYMBOLS = (
     "qrm_last_error", "qrm_abi_version", "qrm_device_count", "qrm_ctx_create", "qrm_ctx_destroy", "qrm_ctx_info",
+    "qrm_ctx_set_extractor",
     "qrm_detect_device", "qrm_detect_host", "qrm_detect_ragged", "qrm_extract_device", "qrm_preprocess_host",
     "qrm_rs_decode_packed_device", "qrm_rs_decode_symbols_device", "qrm_rs_stress_device", "qrm_rs_encode_packed",
     "qrm_verify_threshold", "qrm_make_corpus_device", "qrm_patterns_device", "qrm_allocate_streams",
@@ -62,6 +63,7 @@ RECORD_DTYPE = np.dtype([("raw", "<u8"), ("msg", "<u8"), ("status", "u1"), ("err
 assert RECORD_DTYPE.itemsize == 24
 
 TILE_STRATEGY = {"random": 0, "random_grid": 1, "fixed": 2}
+EXTRACTOR = {"spread_spectrum": 0, "conv": 1}  # QRM_EXTRACTOR_*
 
 
 class _Config(C.Structure):
@@ -95,6 +97,7 @@ def lib() -> C.CDLL:
         L.qrm_ctx_create.argtypes = [i32, C.POINTER(_Config), C.POINTER(vp)]
         L.qrm_ctx_destroy.argtypes = [vp]
         L.qrm_ctx_info.argtypes = [vp, C.POINTER(u64), C.POINTER(u64), C.POINTER(i32), C.POINTER(i32)]
+        L.qrm_ctx_set_extractor.argtypes = [vp, i32, u64]
         L.qrm_detect_device.argtypes = [vp, vp, i64, i32, i32, i64, u64, vp, vp]
         L.qrm_detect_host.argtypes = [vp, vp, i64, i32, i32, i64, u64, vp, C.POINTER(_Plan), i32,
                                       C.POINTER(_HostStats)]
@@ -320,6 +323,11 @@ class DetectionConfig:
     fpr_target: float = 1e-6
     key_message: np.ndarray | None = None
     code: CodeParams | None = field(default=None)
+    # extractor behind the WatermarkCodec plug-in point: "spread_spectrum" (the
+    # reference's SpreadSpectrumCodec) or "conv" (learned conv stack, weights
+    # drawn from conv_seed; oracle/hidden_oracle.c is its contract)
+    extractor: str = "spread_spectrum"
+    conv_seed: int = 7
 
     def __post_init__(self):
         if self.code is None:
@@ -371,8 +379,12 @@ class DetectionContext:
         self.device = device
         h = C.c_void_p()
         c = cfg._c()
+        if cfg.extractor not in EXTRACTOR:
+            raise InvalidInput(f"unknown extractor: {cfg.extractor}")
         _check(lib().qrm_ctx_create(device, C.byref(c), C.byref(h)))
         self._h = h
+        if EXTRACTOR[cfg.extractor]:
+            _check(lib().qrm_ctx_set_extractor(h, EXTRACTOR[cfg.extractor], cfg.conv_seed))  # close() frees h
         cw, msg, tm, tr = C.c_uint64(), C.c_uint64(), C.c_int(), C.c_int()
         _check(lib().qrm_ctx_info(h, C.byref(cw), C.byref(msg), C.byref(tm), C.byref(tr)))
         self.key_codeword, self.key_message, self.tau_message, self.tau_raw = cw.value, msg.value, tm.value, tr.value

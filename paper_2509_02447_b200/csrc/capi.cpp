@@ -167,6 +167,8 @@ struct qrm_ctx {
     std::vector<cudaStream_t> streams;
     qrm_plan plan{{1, 2, 1}, {4096, 4096, 4096}};
     std::unique_ptr<HostPool> pool;  // window staging workers (host pipeline, mode 2)
+    int extractor = QRM_EXTRACTOR_SPREAD_SPECTRUM;  // qrm_ctx_set_extractor
+    uint64_t conv_seed = 7;
     // learned (conv) extractor: folded weights + activation ping-pong buffers
     struct Hidden {
         bool ready = false;
@@ -235,6 +237,9 @@ DetectParams base_params(qrm_ctx* c, Workspace& w, int64_t count, qrm_record* ou
     return p;
 }
 
+qrm_status hidden_run(qrm_ctx* c, Workspace& W, const WindowSource& src, int64_t count, qrm_record* out,
+                      float* logits, cudaStream_t st);
+
 // Decode + correct `count` windows described by src into device records.
 cudaEvent_t g_probe[2] = {nullptr, nullptr};  // set only by qrm_probe_decode_kernel
 
@@ -243,6 +248,15 @@ qrm_status run_detect(qrm_ctx* c, Workspace& w, const WindowSource& src, int64_t
                       cudaStream_t finish_stream = nullptr) {
     qrm_status s = workspace_reserve(w, count);
     if (s != QRM_OK) return s;
+    if (c->extractor == QRM_EXTRACTOR_CONV) {
+        // learned extractor: conv stack + head (+ RS finish) on st
+        if ((s = hidden_run(c, w, src, count, out, nullptr, st)) != QRM_OK) return s;
+        if (mid_event && finish_stream) {
+            QRM_CUDA(cudaEventRecord(mid_event, st));
+            QRM_CUDA(cudaStreamWaitEvent(finish_stream, mid_event, 0));
+        }
+        return QRM_OK;
+    }
     DetectParams p = base_params(c, w, count, out, soft, raw);
     p.src = src;
     if (g_probe[0]) QRM_CUDA(cudaEventRecord(g_probe[0], st));
@@ -654,7 +668,8 @@ QRM_EXPORT qrm_status qrm_detect_host(qrm_ctx* c, const uint8_t* images, int64_t
         const int64_t first = b * mb;
         const int64_t cnt = std::min(mb, count - first);
         cudaStream_t xs = c->streams[b % s0];
-        cudaStream_t ds = c->streams[s0 + b % s1];
+        // the conv extractor's activation buffers are per context: one decode stream
+        cudaStream_t ds = c->streams[s0 + (c->extractor == QRM_EXTRACTOR_CONV ? 0 : b % s1)];
         cudaStream_t cs = c->streams[s0 + s1 + b % s2];
         const int slot = static_cast<int>(b % s1);
         Workspace& W = c->ws[1 + slot];
@@ -942,6 +957,15 @@ qrm_status encode_act_tmap(CUtensorMap* map, CUtensorMap* store_map, void* base,
     return QRM_OK;
 }
 
+// One 64->64 conv layer: single-CTA kernel; QRM_CONV_PAIR=1 selects the CTA-pair
+// (cta_group::2) variant (correct, but measured 11.1 vs 9.8 ms per 4096 tiles).
+cudaError_t conv64_layer(const CUtensorMap& tmap, const CUtensorMap& tmap_out, const HiddenLayerParams& p, int sms,
+                         cudaStream_t st) {
+    const char* e = getenv("QRM_CONV_PAIR");
+    const bool pair = e && e[0] == '1';
+    return pair ? launch_conv64_pair(tmap, tmap_out, p, sms, st) : launch_conv64(tmap, tmap_out, p, sms, st);
+}
+
 qrm_status hidden_prepare(qrm_ctx* c, uint64_t seed, int64_t tiles, cudaStream_t st) {
     auto& H = c->hid;
     if (!H.w_sw) {
@@ -971,6 +995,68 @@ qrm_status hidden_prepare(qrm_ctx* c, uint64_t seed, int64_t tiles, cudaStream_t
     return QRM_OK;
 }
 
+// The windows of images [off, off + n) of a batch source.
+WindowSource slice_source(const WindowSource& src, int64_t off, int K) {
+    WindowSource s = src;
+    if (src.direct) {
+        s.base = src.base + off * src.image_stride;
+        s.first_draw = src.first_draw + static_cast<uint64_t>(off);
+    } else {
+        s.base = src.base + off * static_cast<int64_t>(K);
+    }
+    return s;
+}
+
+// Learned extractor over `count` windows: conv0 -> 8 x conv64 -> head (pool,
+// linear, harden, t = 1 RS + verify) -> finish (general-t codes), in chunks of
+// at most kConvChunk tiles (activation ping-pong buffers: 2 x 512 KB per tile).
+qrm_status hidden_run(qrm_ctx* c, Workspace& W, const WindowSource& src, int64_t count, qrm_record* out,
+                      float* logits, cudaStream_t st) {
+    constexpr int64_t kConvChunk = 8192;
+    if (c->l != 64) return fail(QRM_INVALID_INPUT, "the conv extractor is defined on 64x64 tiles");
+    qrm_status s;
+    if ((s = hidden_prepare(c, c->conv_seed, std::min(count, kConvChunk), st)) != QRM_OK) return s;
+    auto& H = c->hid;
+    for (int64_t off = 0; off < count; off += kConvChunk) {
+        const int64_t n = std::min(kConvChunk, count - off);
+        const WindowSource cs = slice_source(src, off, c->K);
+        Conv0Params p0{cs, n, c->K, H.w0, H.bias, H.act[0]};
+        QRM_LAUNCH(launch_conv0(p0, H.tmap_st[0], c->sms, st));
+        for (int j = 1; j < kHiddenLayers; ++j) {
+            HiddenLayerParams lp{};
+            lp.w_swizzled = H.w_sw + static_cast<int64_t>(j - 1) * 9 * 64 * 64;
+            lp.bias = H.bias + j * 64;
+            lp.last = j == kHiddenLayers - 1;
+            lp.act_out = lp.last ? nullptr : H.act[j & 1];
+            lp.pool_out = lp.last ? H.pool : nullptr;
+            lp.tiles = n;
+            QRM_LAUNCH(conv64_layer(H.tmap[(j - 1) & 1], H.tmap_st[j & 1], lp, c->sms, st));
+        }
+        HeadParams hp{};
+        hp.pool = H.pool;
+        hp.wl = H.wl;
+        hp.bl = H.bl;
+        hp.tiles = n;
+        hp.nbits = c->nbits;
+        hp.kbits = c->kbits;
+        hp.tau_msg = c->tau_msg;
+        hp.tau_raw = c->tau_raw;
+        hp.fuse_t1 = (c->t == 1 && c->n - c->k <= 3) ? 1 : 0;
+        hp.key_cw = c->key_cw;
+        hp.key_msg = c->key_msg;
+        hp.rs = c->d_rs;
+        hp.logits = logits ? logits + off * c->nbits : nullptr;
+        hp.out = out + off;
+        hp.pending_count = W.pending_count;
+        hp.pending = W.pending;
+        QRM_LAUNCH(launch_hidden_head(hp, st));
+        DetectParams fp = base_params(c, W, n, out + off, nullptr, nullptr);
+        fp.src = cs;
+        QRM_LAUNCH(launch_detect_finish(fp, std::max(1, c->t), c->sms, st));  // general-t codes only
+    }
+    return QRM_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -982,49 +1068,28 @@ QRM_EXPORT qrm_status qrm_hidden_detect_device(qrm_ctx* c, const uint8_t* images
     if (s != QRM_OK) return s;
     if (count > 0 && !out) return fail(QRM_INVALID_INPUT, "null record buffer");
     if (c->l != 64) return fail(QRM_INVALID_INPUT, "the conv extractor is defined on 64x64 tiles");
-    if (count >= (int64_t{1} << 19)) return fail(QRM_INVALID_INPUT, "conv extractor batch must be < 524288 tiles");
     if ((s = set_device(c->device)) != QRM_OK) return s;
     if (count == 0) return QRM_OK;
     cudaStream_t st = as_stream(stream);
     Workspace& W = c->ws[0];
-    if ((s = hidden_prepare(c, weight_seed, count, st)) != QRM_OK) return s;
+    const uint64_t keep = c->conv_seed;
+    c->conv_seed = weight_seed;
     if ((s = workspace_reserve(W, count)) != QRM_OK) return s;
     WindowSource src;
-    if ((s = window_source(c, W, images, count, w, h, stride, first_draw, st, src)) != QRM_OK) return s;
-    auto& H = c->hid;
-    Conv0Params p0{src, count, c->K, H.w0, H.bias, H.act[0]};
-    QRM_LAUNCH(launch_conv0(p0, H.tmap_st[0], c->sms, st));
-    for (int j = 1; j < kHiddenLayers; ++j) {
-        HiddenLayerParams lp{};
-        lp.w_swizzled = H.w_sw + static_cast<int64_t>(j - 1) * 9 * 64 * 64;
-        lp.bias = H.bias + j * 64;
-        lp.last = j == kHiddenLayers - 1;
-        lp.act_out = lp.last ? nullptr : H.act[j & 1];
-        lp.pool_out = lp.last ? H.pool : nullptr;
-        lp.tiles = count;
-        QRM_LAUNCH(launch_conv64(H.tmap[(j - 1) & 1], H.tmap_st[j & 1], lp, c->sms, st));
-    }
-    HeadParams hp{};
-    hp.pool = H.pool;
-    hp.wl = H.wl;
-    hp.bl = H.bl;
-    hp.tiles = count;
-    hp.nbits = c->nbits;
-    hp.kbits = c->kbits;
-    hp.tau_msg = c->tau_msg;
-    hp.tau_raw = c->tau_raw;
-    hp.fuse_t1 = (c->t == 1 && c->n - c->k <= 3) ? 1 : 0;
-    hp.key_cw = c->key_cw;
-    hp.key_msg = c->key_msg;
-    hp.rs = c->d_rs;
-    hp.logits = logits;
-    hp.out = out;
-    hp.pending_count = W.pending_count;
-    hp.pending = W.pending;
-    QRM_LAUNCH(launch_hidden_head(hp, st));
-    DetectParams fp = base_params(c, W, count, out, nullptr, nullptr);
-    fp.src = src;
-    QRM_LAUNCH(launch_detect_finish(fp, std::max(1, c->t), c->sms, st));  // general-t codes only
+    if ((s = window_source(c, W, images, count, w, h, stride, first_draw, st, src)) == QRM_OK)
+        s = hidden_run(c, W, src, count, out, logits, st);
+    c->conv_seed = keep;
+    return s;
+}
+
+QRM_EXPORT qrm_status qrm_ctx_set_extractor(qrm_ctx* c, int kind, uint64_t weight_seed) {
+    if (!c) return fail(QRM_INVALID_INPUT, "null context");
+    if (kind != QRM_EXTRACTOR_SPREAD_SPECTRUM && kind != QRM_EXTRACTOR_CONV)
+        return fail(QRM_INVALID_INPUT, "unknown extractor kind");
+    if (kind == QRM_EXTRACTOR_CONV && c->l != 64)
+        return fail(QRM_INVALID_INPUT, "the conv extractor is defined on 64x64 tiles");
+    c->extractor = kind;
+    c->conv_seed = weight_seed;
     return QRM_OK;
 }
 
@@ -1053,7 +1118,7 @@ QRM_EXPORT qrm_status qrm_hidden_debug_activation(qrm_ctx* c, const uint8_t* ima
         lp.pool_out = lp.last ? H.pool : nullptr;
         lp.tiles = count;
         if (const char* e = getenv("QRM_HIDDEN_DBG")) lp.dbg = atoi(e);
-        QRM_LAUNCH(launch_conv64(H.tmap[(j - 1) & 1], H.tmap_st[j & 1], lp, c->sms, st));
+        QRM_LAUNCH(conv64_layer(H.tmap[(j - 1) & 1], H.tmap_st[j & 1], lp, c->sms, st));
     }
     if (stop_after == kHiddenLayers - 1)
         QRM_CUDA(cudaMemcpyAsync(out, H.pool, sizeof(float) * kHiddenBlocksPerTile * 64 * count,

@@ -721,7 +721,11 @@ DetectionContext::DetectionContext(const DetectionConfig& cfg, int device)
     if (cfg.rs_workers < 1) throw InvalidInput("rs_workers must be >= 1");
     if (cfg.fpr_target <= 0.0 || cfg.fpr_target >= 1.0) throw InvalidInput("fpr target must be in (0, 1)");
     qrm_config c = gpu_config(cfg_);
-    const qrm_status s = qrm_ctx_create(device, &c, &gpu_->h);
+    qrm_status s = qrm_ctx_create(device, &c, &gpu_->h);
+    if (s == QRM_OK && cfg.extractor == ExtractorKind::conv) {
+        s = qrm_ctx_set_extractor(gpu_->h, QRM_EXTRACTOR_CONV, cfg.conv_weight_seed);
+        if (s != QRM_OK) qrm_ctx_destroy(gpu_->h);
+    }
     if (s != QRM_OK) {
         delete gpu_;
         raise(s);

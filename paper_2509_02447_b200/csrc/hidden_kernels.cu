@@ -43,11 +43,12 @@ constexpr int kHWBytes = 9 * kHC * kHC * 2;  // 73,728 B of bf16 weights per lay
 constexpr int kHABytes = 4 * kHSide * kHC * 2;  // 32 KB: 4 input rows
 constexpr int kHAStages = 4;
 constexpr int kHThreads = 192;             // warp 0 TMA, warp 1 MMA, warps 2-5 epilogue
+constexpr int kHAcc = 4;                   // TMEM accumulator buffers (64 columns each)
 
 struct HiddenSmem {
     uint64_t w_full;
     uint64_t a_full[kHAStages], a_empty[kHAStages];
-    uint64_t acc_full[2], acc_empty[2];
+    uint64_t acc_full[kHAcc], acc_empty[kHAcc];
     uint32_t tmem_base;
     float pool[4][kHC];  // per-epilogue-warp channel sums (last layer)
 };
@@ -56,6 +57,71 @@ constexpr int kHOBytes = 4 * 32 * kHC * 2;  // 16 KB: output staging, 4 KB per e
 // slack; views may read <= 128 B outside an A buffer; those rows are masked lanes)
 constexpr size_t kHSmemBytes = 1024 + kHWBytes + kHAStages * kHABytes + kHOBytes + 128 + sizeof(HiddenSmem);
 static_assert(kHSmemBytes <= 232448, "conv64 shared memory exceeds 227 KB");
+
+// Epilogue of one 128-pixel block (32 pixels per warp, one per lane): bias +
+// ReLU, then either bf16 NHWC rows -> 128B-swizzled per-warp slab -> one TMA
+// store, or (last layer) the block's per-channel sums for the average pool.
+__device__ __forceinline__ void conv_epilogue(const HiddenLayerParams& p, const CUtensorMap* tmap_out,
+                                              const uint32_t (&acc)[kHC], const float* s_bias, float (*pool)[kHC],
+                                              uint32_t o_s, int q, int lane, int64_t tile, int blk) {
+    const int pix = blk * kHM + q * 32 + lane;
+    float v[kHC];
+#pragma unroll
+    for (int c = 0; c < kHC; ++c) v[c] = fmaxf(__uint_as_float(acc[c]) + s_bias[c], 0.0f);
+    if (!p.last) {
+        // Stage this warp's 32 pixels x 128 B as a 128B-swizzled slab (16-B
+        // chunk c of row r at chunk c ^ (r & 7): conflict free), then one TMA
+        // store writes the 4 KB contiguous NHWC run.
+        const uint32_t slab = o_s + q * 4096;
+        if (lane == 0) bulk_wait_read<0>();  // previous store has read the slab
+        __syncwarp();
+        const uint32_t row = slab + lane * 128;
+#pragma unroll
+        for (int c = 0; c < kHC; c += 8) {
+            uint4 o;
+            __nv_bfloat162 h0 = __floats2bfloat162_rn(v[c], v[c + 1]);
+            __nv_bfloat162 h1 = __floats2bfloat162_rn(v[c + 2], v[c + 3]);
+            __nv_bfloat162 h2 = __floats2bfloat162_rn(v[c + 4], v[c + 5]);
+            __nv_bfloat162 h3 = __floats2bfloat162_rn(v[c + 6], v[c + 7]);
+            o.x = *reinterpret_cast<uint32_t*>(&h0);
+            o.y = *reinterpret_cast<uint32_t*>(&h1);
+            o.z = *reinterpret_cast<uint32_t*>(&h2);
+            o.w = *reinterpret_cast<uint32_t*>(&h3);
+            st_shared_v4(row + ((((c >> 3) ^ lane) & 7) << 4), o);
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+            tma_store_2d(tmap_out, slab, 0, static_cast<int>(tile * kHPix + pix - lane));
+            bulk_commit();
+        }
+    } else {
+        // Average pool, part 1: channel sums over this warp's 32 pixels by
+        // recursive halving (each step a lane keeps half the channels).
+#pragma unroll
+        for (int o = 16, n = kHC / 2; o >= 1; o >>= 1, n >>= 1) {
+            const bool upper = (lane & o) != 0;
+#pragma unroll
+            for (int c = 0; c < n; ++c) {
+                const float send = upper ? v[c] : v[c + n];
+                const float keep = upper ? v[c + n] : v[c];
+                v[c] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+            }
+        }
+        // Step o kept the upper half iff lane bit log2(o) is set, adding
+        // 2*o to the channel base: lane L now holds channels 2L, 2L+1.
+        pool[q][2 * lane] = v[0];
+        pool[q][2 * lane + 1] = v[1];
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (q == 0 && lane < kHC / 2) {
+            // part 2: fixed-order sum of the 4 warps -> per-block partial
+            for (int c2 = lane * 2; c2 < lane * 2 + 2; ++c2)
+                p.pool_out[(tile * kHBlocks + blk) * kHC + c2] =
+                    ((pool[0][c2] + pool[1][c2]) + pool[2][c2]) + pool[3][c2];
+        }
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+    }
+}
 
 __global__ void __launch_bounds__(kHThreads, 1)
     conv64_kernel(const __grid_constant__ CUtensorMap tmap_in, const __grid_constant__ CUtensorMap tmap_out,
@@ -71,14 +137,14 @@ __global__ void __launch_bounds__(kHThreads, 1)
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int64_t nblocks = p.tiles * kHBlocks;
 
-    if (warp == 1) tmem_alloc<128>(&sm.tmem_base);
+    if (warp == 1) tmem_alloc<kHAcc * kHC>(&sm.tmem_base);
     if (tid == 0) {
         mbar_init(&sm.w_full, 1);
         for (int s = 0; s < kHAStages; ++s) {
             mbar_init(&sm.a_full[s], 1);
             mbar_init(&sm.a_empty[s], 1);
         }
-        for (int a = 0; a < 2; ++a) {
+        for (int a = 0; a < kHAcc; ++a) {
             mbar_init(&sm.acc_full[a], 1);
             mbar_init(&sm.acc_empty[a], 4);
         }
@@ -115,9 +181,9 @@ __global__ void __launch_bounds__(kHThreads, 1)
         mbar_wait(&sm.w_full, 0);
         int i = 0;
         for (int64_t b = blockIdx.x; b < nblocks; b += gridDim.x, ++i) {
-            const int s = i % kHAStages, a = i & 1;
+            const int s = i % kHAStages, a = i % kHAcc;
             mbar_wait(&sm.a_full[s], (i / kHAStages) & 1);
-            mbar_wait(&sm.acc_empty[a], ((i >> 1) & 1) ^ 1);
+            mbar_wait(&sm.acc_empty[a], ((i / kHAcc) & 1) ^ 1);
             tc_fence_after();
             const uint32_t d = tmem + a * kHC;
             const uint64_t da0 = sw128_kmajor_desc(a_s0 + s * kHABytes);
@@ -150,8 +216,8 @@ __global__ void __launch_bounds__(kHThreads, 1)
         const int q = warp & 3;  // TMEM lane quarter this warp may access
         int i = 0;
         for (int64_t b = blockIdx.x; b < nblocks; b += gridDim.x, ++i) {
-            const int a = i & 1;
-            mbar_wait(&sm.acc_full[a], (i >> 1) & 1);
+            const int a = i % kHAcc;
+            mbar_wait(&sm.acc_full[a], (i / kHAcc) & 1);
             tc_fence_after();
             uint32_t acc[kHC];
 #pragma unroll
@@ -165,71 +231,170 @@ __global__ void __launch_bounds__(kHThreads, 1)
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&sm.acc_empty[a]);
-            const int64_t tile = b / kHBlocks;
-            const int pix = static_cast<int>(b % kHBlocks) * kHM + q * 32 + lane;
-            float v[kHC];
-#pragma unroll
-            for (int c = 0; c < kHC; ++c) v[c] = fmaxf(__uint_as_float(acc[c]) + s_bias[c], 0.0f);
-            if (!p.last) {
-                // Stage this warp's 32 pixels x 128 B as a 128B-swizzled slab (16-B
-                // chunk c of row r at chunk c ^ (r & 7): conflict free), then one TMA
-                // store writes the 4 KB contiguous NHWC run.
-                const uint32_t slab = o_s + q * 4096;
-                if (lane == 0) bulk_wait_read<0>();  // previous store has read the slab
-                __syncwarp();
-                const uint32_t row = slab + lane * 128;
-#pragma unroll
-                for (int c = 0; c < kHC; c += 8) {
-                    uint4 o;
-                    __nv_bfloat162 h0 = __floats2bfloat162_rn(v[c], v[c + 1]);
-                    __nv_bfloat162 h1 = __floats2bfloat162_rn(v[c + 2], v[c + 3]);
-                    __nv_bfloat162 h2 = __floats2bfloat162_rn(v[c + 4], v[c + 5]);
-                    __nv_bfloat162 h3 = __floats2bfloat162_rn(v[c + 6], v[c + 7]);
-                    o.x = *reinterpret_cast<uint32_t*>(&h0);
-                    o.y = *reinterpret_cast<uint32_t*>(&h1);
-                    o.z = *reinterpret_cast<uint32_t*>(&h2);
-                    o.w = *reinterpret_cast<uint32_t*>(&h3);
-                    st_shared_v4(row + ((((c >> 3) ^ lane) & 7) << 4), o);
-                }
-                fence_proxy_async_smem();
-                __syncwarp();
-                if (lane == 0) {
-                    tma_store_2d(&tmap_out, slab, 0, static_cast<int>(tile * kHPix + pix - lane));
-                    bulk_commit();
-                }
-            } else {
-                // Average pool, part 1: channel sums over this warp's 32 pixels by
-                // recursive halving (each step a lane keeps half the channels).
-#pragma unroll
-                for (int o = 16, n = kHC / 2; o >= 1; o >>= 1, n >>= 1) {
-                    const bool upper = (lane & o) != 0;
-#pragma unroll
-                    for (int c = 0; c < n; ++c) {
-                        const float send = upper ? v[c] : v[c + n];
-                        const float keep = upper ? v[c + n] : v[c];
-                        v[c] = keep + __shfl_xor_sync(0xffffffffu, send, o);
-                    }
-                }
-                // Step o kept the upper half iff lane bit log2(o) is set, adding
-                // 2*o to the channel base: lane L now holds channels 2L, 2L+1.
-                sm.pool[q][2 * lane] = v[0];
-                sm.pool[q][2 * lane + 1] = v[1];
-                asm volatile("bar.sync 1, 128;" ::: "memory");
-                if (q == 0 && lane < kHC / 2) {
-                    // part 2: fixed-order sum of the 4 warps -> per-block partial
-                    for (int c2 = lane * 2; c2 < lane * 2 + 2; ++c2)
-                        p.pool_out[(tile * kHBlocks + b % kHBlocks) * kHC + c2] =
-                            ((sm.pool[0][c2] + sm.pool[1][c2]) + sm.pool[2][c2]) + sm.pool[3][c2];
-                }
-                asm volatile("bar.sync 1, 128;" ::: "memory");
-            }
+            conv_epilogue(p, &tmap_out, acc, s_bias, sm.pool, o_s, q, lane, b / kHBlocks, static_cast<int>(b % kHBlocks));
         }
         if (!p.last && lane == 0) bulk_wait<0>();
     }
     __syncthreads();
     if (warp == 1) {
         tc_fence_after();
-        tmem_dealloc<128>(tmem);
+        tmem_dealloc<kHAcc * kHC>(tmem);
+    }
+}
+
+
+// conv64_pair_kernel — the same layer on CTA pairs (cluster of 2, cta_group::2).
+// A pair-block is 256 output pixels = 4 image rows of one tile: CTA r holds
+// rows y0+2r, y0+2r+1 (its own 4-row TMA window, as conv64_kernel) and half of
+// the folded weights (output channels 32r..32r+31, 36 KB). The even CTA issues
+// M=256 x N=64 x K=16 MMAs that read A rows 0-127 / 128-255 and the two weight
+// halves from the two CTAs' smem, and each CTA's TMEM receives its 128 rows x
+// 64 channels. Per-CTA operand traffic per MMA falls from 4 KB A + 2 KB B to
+// 4 KB A + 1 KB B, and the freed weight smem buys a 5th A stage.
+//   full[s]     (even CTA)  2 arrivals (+tx): both CTAs' TMA windows landed
+//   empty[s]    (each CTA)  multicast commit of the pair's MMAs
+//   acc_full[a] (each CTA)  multicast commit
+//   acc_empty[a](even CTA)  8 arrivals: the 4 epilogue warps of both CTAs
+constexpr int kPWBytes = kHWBytes / 2;  // 36 KB: 9 taps x 32 co x 64 ci
+constexpr int kPAStages = 5;
+struct PairSmem {
+    uint64_t w_full;
+    uint64_t a_full[kPAStages], a_empty[kPAStages];
+    uint64_t acc_full[kHAcc], acc_empty[kHAcc];
+    uint32_t tmem_base;
+    float pool[4][kHC];
+};
+constexpr size_t kPSmemBytes = 1024 + kPWBytes + kPAStages * kHABytes + kHOBytes + 128 + sizeof(PairSmem);
+static_assert(kPSmemBytes <= 232448, "conv64 pair shared memory exceeds 227 KB");
+constexpr int kPairBlocks = kHBlocks / 2;  // 16 pair-blocks (4 rows) per tile
+
+__global__ void __launch_bounds__(kHThreads, 1)
+    conv64_pair_kernel(const __grid_constant__ CUtensorMap tmap_in, const __grid_constant__ CUtensorMap tmap_out,
+                       const __grid_constant__ HiddenLayerParams p) {
+    extern __shared__ uint8_t smem_raw[];
+    __shared__ float s_bias[kHC];
+    uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const uint32_t w_s = smem_u32(base);
+    const uint32_t a_s0 = w_s + kPWBytes;
+    const uint32_t o_s = a_s0 + kPAStages * kHABytes;
+    PairSmem& sm = *reinterpret_cast<PairSmem*>(base + kPWBytes + kPAStages * kHABytes + kHOBytes + 128);
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const uint32_t rank = cluster_ctarank();  // 0 = even CTA (MMA issuer), 1 = odd
+    const int64_t npb = p.tiles * kPairBlocks;
+    const int64_t pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+
+    if (warp == 1) tmem_alloc_pair<kHAcc * kHC>(&sm.tmem_base);
+    if (tid == 0) {
+        mbar_init(&sm.w_full, 1);
+        for (int s = 0; s < kPAStages; ++s) {
+            mbar_init(&sm.a_full[s], 2);
+            mbar_init(&sm.a_empty[s], 1);
+        }
+        for (int a = 0; a < kHAcc; ++a) {
+            mbar_init(&sm.acc_full[a], 1);
+            mbar_init(&sm.acc_empty[a], 8);
+        }
+        mbar_fence_init();
+    }
+    if (tid < kHC) s_bias[tid] = p.bias[tid];
+    tc_fence_before();
+    cluster_sync_all();  // barriers initialised in both CTAs before any remote arrive
+    tc_fence_after();
+    const uint32_t tmem = sm.tmem_base;
+
+    // Barrier phase 2 ("both weight halves resident"): the TMA warp arrives at
+    // once and waits only after its loop; the MMA warp waits before its first MMA.
+    if (warp == 0) {
+        // ---------------------------------------------------------- TMA ----
+        cluster_arrive();
+        if (lane == 0) {
+            // this CTA's weight half: output channels 32r..32r+31 of every tap
+            mbar_arrive_expect_tx(&sm.w_full, kPWBytes);
+            for (int t = 0; t < 9; ++t)
+                bulk_load(w_s + t * 4096, p.w_swizzled + (t * kHC + 32 * rank) * kHC, 4096, &sm.w_full);
+            int i = 0;
+            for (int64_t b = pair; b < npb; b += npairs, ++i) {
+                const int s = i % kPAStages;
+                mbar_wait(&sm.a_empty[s], ((i / kPAStages) & 1) ^ 1);
+                const int tile = static_cast<int>(b / kPairBlocks);
+                const int y0 = static_cast<int>(b % kPairBlocks) * 4 + 2 * static_cast<int>(rank);
+                const uint32_t full0 = map_to_rank(smem_u32(&sm.a_full[s]), 0);
+                mbar_arrive_expect_tx_cluster(full0, kHABytes);
+                tma_load_4d_pair(a_s0 + s * kHABytes, &tmap_in, 0, 0, y0 - 1, tile, full0);
+            }
+        }
+    } else if (warp == 1) {
+        // ---------------------------------------------------------- MMA ----
+        mbar_wait(&sm.w_full, 0);
+        cluster_sync_all();  // both weight halves resident
+        if (rank == 0) {
+            const uint32_t idesc = idesc_bf16_f32(2 * kHM, kHC);
+            const uint64_t db0 = sw128_kmajor_desc(w_s);
+            int i = 0;
+            for (int64_t b = pair; b < npb; b += npairs, ++i) {
+                const int s = i % kPAStages, a = i % kHAcc;
+                mbar_wait(&sm.a_full[s], (i / kPAStages) & 1);
+                mbar_wait(&sm.acc_empty[a], ((i / kHAcc) & 1) ^ 1);
+                tc_fence_after();
+                const uint32_t d = tmem + a * kHC;
+                const uint64_t da0 = sw128_kmajor_desc(a_s0 + s * kHABytes);
+                if (elect_one()) {
+#pragma unroll
+                    for (int t = 0; t < 9; ++t) {
+                        const int tap = t == 0 ? 4 : (t <= 4 ? t - 1 : t);  // centre tap first (no mask)
+                        const int dy = tap / 3 - 1, dx = tap % 3 - 1;
+                        const int view = (64 * (1 + dy) + dx) * 128;
+                        const uint32_t m0 = dx < 0 ? 1u : 0u, m1 = dx > 0 ? 0x80000000u : 0u;
+#pragma unroll
+                        for (int k = 0; k < 4; ++k) {
+                            const uint64_t da = da0 + static_cast<uint64_t>(static_cast<int64_t>((view + 32 * k) >> 4));
+                            const uint64_t db = db0 + static_cast<uint64_t>((tap * 4096 + 32 * k) >> 4);
+                            umma_bf16_pair_masked(d, da, db, idesc, (t | k) != 0, m0, m1);
+                        }
+                    }
+                    umma_commit_pair_mc(&sm.a_empty[s], 0x3);
+                    umma_commit_pair_mc(&sm.acc_full[a], 0x3);
+                }
+                __syncwarp();
+            }
+        }
+    } else {
+        // ----------------------------------------------------- epilogue ----
+        cluster_sync_all();
+        const int q = warp & 3;
+        uint32_t empty0[kHAcc];
+#pragma unroll
+        for (int a = 0; a < kHAcc; ++a) empty0[a] = map_to_rank(smem_u32(&sm.acc_empty[a]), 0);
+        int i = 0;
+        for (int64_t b = pair; b < npb; b += npairs, ++i) {
+            const int a = i % kHAcc;
+            mbar_wait(&sm.acc_full[a], (i / kHAcc) & 1);
+            tc_fence_after();
+            uint32_t acc[kHC];
+#pragma unroll
+            for (int c = 0; c < kHC / 16; ++c) {
+                uint32_t r16[16];
+                tmem_ld16(tmem + (static_cast<uint32_t>(q * 32) << 16) + a * kHC + c * 16, r16);
+#pragma unroll
+                for (int j = 0; j < 16; ++j) acc[c * 16 + j] = r16[j];
+            }
+            tmem_ld_wait();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster(empty0[a]);
+            conv_epilogue(p, &tmap_out, acc, s_bias, sm.pool, o_s, q, lane, b / kPairBlocks,
+                          static_cast<int>(b % kPairBlocks) * 2 + static_cast<int>(rank));
+        }
+        if (!p.last && lane == 0) bulk_wait<0>();
+    }
+    __syncwarp();
+    if (warp == 0) cluster_wait();  // the TMA warp's wait of barrier phase 2
+    tc_fence_before();
+    cluster_sync_all();  // both CTAs done with TMEM and with each other's smem
+    if (warp == 1) {
+        tc_fence_after();
+        tmem_dealloc_pair<kHAcc * kHC>(tmem);
     }
 }
 
@@ -528,6 +693,34 @@ cudaError_t launch_conv64(const CUtensorMap& tmap, const CUtensorMap& tmap_out, 
     if (grid > nblocks) grid = nblocks;
     conv64_kernel<<<static_cast<unsigned>(grid), kHThreads, kHSmemBytes, st>>>(tmap, tmap_out, p);
     return cudaGetLastError();
+}
+
+
+cudaError_t launch_conv64_pair(const CUtensorMap& tmap, const CUtensorMap& tmap_out, const HiddenLayerParams& p,
+                               int sm_count, cudaStream_t st) {
+    static bool configured = false;
+    if (!configured) {
+        cudaError_t e = cudaFuncSetAttribute(conv64_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             static_cast<int>(kPSmemBytes));
+        if (e != cudaSuccess) return e;
+        configured = true;
+    }
+    const int64_t npb = p.tiles * kPairBlocks;
+    int64_t pairs = (sm_count > 0 ? sm_count : 148) / 2;
+    if (pairs > npb) pairs = npb;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(static_cast<unsigned>(2 * pairs));
+    cfg.blockDim = dim3(kHThreads);
+    cfg.dynamicSmemBytes = kPSmemBytes;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, conv64_pair_kernel, tmap, tmap_out, p);
 }
 
 cudaError_t launch_hidden_head(const HeadParams& p, cudaStream_t st) {

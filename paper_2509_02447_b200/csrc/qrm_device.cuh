@@ -311,6 +311,9 @@ QRM_D uint32_t cluster_nctarank() {
 QRM_D void cluster_sync_all() {
     asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
+// Split cluster barrier (a thread may do work between its arrive and its wait).
+QRM_D void cluster_arrive() { asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory"); }
+QRM_D void cluster_wait() { asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory"); }
 // Address of the same shared-memory offset in CTA `rank` of the cluster.
 QRM_D uint32_t map_to_rank(uint32_t smem_addr, uint32_t rank) {
     uint32_t r;
@@ -320,6 +323,62 @@ QRM_D uint32_t map_to_rank(uint32_t smem_addr, uint32_t rank) {
 QRM_D void st_cluster_v4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
     asm volatile("st.shared::cluster.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d)
                  : "memory");
+}
+
+
+// -------------------------------------------------- CTA pair (cta_group::2) ----
+// Both CTAs of the pair execute alloc/dealloc from the same warp; the column
+// range is mirrored in the two TMEMs.
+template <uint32_t kCols>
+QRM_D void tmem_alloc_pair(uint32_t* dst_smem_slot) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(dst_smem_slot)),
+                 "n"(kCols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+}
+template <uint32_t kCols>
+QRM_D void tmem_dealloc_pair(uint32_t taddr) {
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "n"(kCols) : "memory");
+}
+// D[256 x N] (+)= A[256 x K] * B[K x N] over the pair (issued by the even CTA):
+// A rows 0-127 / 128-255 and B columns 0..N/2-1 / N/2..N-1 come from the same
+// smem offsets of CTA 0 / CTA 1; D rows land in each CTA's own TMEM. Eight
+// 32-lane disable masks cover the 256 output rows.
+QRM_D void umma_bf16_pair_masked(uint32_t tmem_d, uint64_t desc_a, uint64_t desc_b, uint32_t idesc,
+                                 uint32_t accumulate, uint32_t m0, uint32_t m1) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, {%5, %6, %5, %6, %5, %6, %5, %6}, p;\n\t}" ::"r"(tmem_d),
+        "l"(desc_a), "l"(desc_b), "r"(idesc), "r"(accumulate), "r"(m0), "r"(m1)
+        : "memory");
+}
+// Commit of the pair's MMAs, arriving once on the barrier at this smem offset
+// in every CTA of `mask`.
+QRM_D void umma_commit_pair_mc(uint64_t* bar, uint16_t mask) {
+    asm volatile(
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+            smem_u32(bar)),
+        "h"(mask)
+        : "memory");
+}
+// Arrive on an mbarrier of another CTA of the cluster (address from map_to_rank).
+QRM_D void mbar_arrive_cluster(uint32_t cluster_addr) {
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+QRM_D void mbar_arrive_expect_tx_cluster(uint32_t cluster_addr, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.release.cluster.shared::cluster.b64 _, [%0], %1;" ::"r"(cluster_addr),
+                 "r"(bytes)
+                 : "memory");
+}
+// 4-D TMA load into this CTA's smem whose completion is signalled on a barrier
+// of either CTA of the pair (cluster address).
+QRM_D void tma_load_4d_pair(uint32_t dst_smem, const void* tmap, int c0, int c1, int c2, int c3, uint32_t bar_cluster) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
+        "%3, %4, %5}], [%6];" ::"r"(dst_smem),
+        "l"(tmap), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(bar_cluster)
+        : "memory");
 }
 
 // Byte offset of 16-byte chunk `c` of row `r` inside a 128B-swizzled K-major tile.

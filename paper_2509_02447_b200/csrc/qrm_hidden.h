@@ -53,6 +53,9 @@ cudaError_t launch_conv0(const Conv0Params& p, const CUtensorMap& tmap_out, int 
 // output activations ({64 ch, T*4096 px}, box {64, 32}, 128B swizzle).
 cudaError_t launch_conv64(const CUtensorMap& tmap, const CUtensorMap& tmap_out, const HiddenLayerParams& p,
                           int sm_count, cudaStream_t st);
+// Same layer on CTA pairs (cluster of 2, cta_group::2 MMAs, M = 256).
+cudaError_t launch_conv64_pair(const CUtensorMap& tmap, const CUtensorMap& tmap_out, const HiddenLayerParams& p,
+                               int sm_count, cudaStream_t st);
 cudaError_t launch_hidden_head(const HeadParams& p, cudaStream_t st);
 
 }  // namespace qrm

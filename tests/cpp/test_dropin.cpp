@@ -375,6 +375,39 @@ static void gpu_stego_detect() {
     for (size_t i = 0; i < rr.size(); ++i) CHECK(semantic_equal(rr[i], rp[i]));
 }
 
+// The learned extractor through the same entry points (DetectionConfig::extractor).
+static void gpu_conv_detect() {
+    CodeParams code = resolve_profile("gf16-15-12");
+    BitVec msg(48);
+    for (int i = 0; i < 48; ++i) msg[i] = rng_word(1, 0x6d73, i) & 1;
+    DetectionConfig cfg = DetectionConfig::make(code, TileSpec{64, TileStrategy::random_grid, 0}, 1, 0.04, msg);
+    cfg.extractor = ExtractorKind::conv;
+    cfg.conv_weight_seed = 7;
+    std::vector<ImageBuffer> imgs;
+    for (int i = 0; i < 12; ++i) imgs.push_back(synthetic_image(1000 + i, 256, 256));
+    auto r1 = detect_batch(imgs, cfg);
+    StreamPlan plan{{1, 2, 1}, {5, 5, 5}, 0.0};
+    auto r2 = detect_batch(imgs, cfg, &plan);
+    DetectionContext ctx(cfg);
+    CHECK(r1.size() == imgs.size());
+    BitVec kcw = rs_encode(msg, code);
+    for (size_t i = 0; i < r1.size(); ++i) {
+        CHECK(semantic_equal(r1[i], r2[i]));
+        CHECK(semantic_equal(r1[i], ctx.detect_one(imgs[i], i)));
+        // RS + verify on the extractor's own hard bits equal the reference chain
+        auto d = bw_decode(r1[i].raw_bits, code);
+        CHECK(d.has_value() == r1[i].corrected.has_value());
+        if (d) CHECK(*r1[i].corrected == d->message && r1[i].errors_corrected == d->errors_corrected);
+        CHECK(r1[i].bit_acc == bit_accuracy(r1[i].raw_bits, kcw));
+    }
+    // the spread-spectrum default is unaffected by a conv context alive beside it
+    cfg.extractor = ExtractorKind::spread_spectrum;
+    auto r3 = detect_batch(imgs, cfg);
+    bool differs = false;
+    for (size_t i = 0; i < r3.size(); ++i) differs |= r3[i].raw_bits != r1[i].raw_bits;
+    CHECK(differs);
+}
+
 int main(int argc, char** argv) {
     const std::string which = argc > 1 ? argv[1] : "all";
     struct Case {
@@ -383,7 +416,8 @@ int main(int argc, char** argv) {
         void (*fn)();
     } cases[] = {{"gf", false, host_gf},          {"rs_encode", false, host_rs_encode},
                  {"tiling_sched", false, host_tiling_sched}, {"rs_gpu", true, gpu_rs},
-                 {"image_gpu", true, gpu_image},  {"stego_detect_gpu", true, gpu_stego_detect}};
+                 {"image_gpu", true, gpu_image},  {"stego_detect_gpu", true, gpu_stego_detect},
+                 {"conv_detect_gpu", true, gpu_conv_detect}};
     for (auto& c : cases) {
         if ((which == "host" && c.gpu) || (which == "gpu" && !c.gpu)) continue;
         const int before = g_fail;

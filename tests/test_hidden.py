@@ -81,3 +81,44 @@ def test_conv_extractor_matches_oracle(qrm, cuda, orc):
             assert bool(rec["verified"][i]) == (int((res[0] == key).sum()) >= 41)
         else:
             assert bool(rec["verified"][i]) == (matches >= 49)
+
+
+@pytest.mark.gpu
+def test_conv_pair_variant_matches_single(qrm, cuda, monkeypatch):
+    """The CTA-pair (cta_group::2, M=256) conv layer gives the same logits as the
+    single-CTA layer: identical bf16 products, fp32 accumulation in the same
+    tap/K order per output pixel, so the results agree to fp32 rounding."""
+    cfg = qrm.DetectionConfig()
+    imgs = cuda.cat([qrm.make_corpus(cfg, 1000, 40), qrm.make_corpus(cfg, 5000, 40, embed=False)])
+    out = {}
+    for pair in ("0", "1"):
+        monkeypatch.setenv("QRM_CONV_PAIR", pair)
+        with qrm.DetectionContext(cfg) as ctx:
+            lg, rec = ctx.hidden_detect_device(imgs, weight_seed=SEED, first_draw=11)
+            cuda.cuda.synchronize()
+        out[pair] = (lg.cpu().numpy(), qrm.records_from_device(rec))
+    a, b = out["0"][0], out["1"][0]
+    assert np.max(np.abs(a - b)) <= 1e-5 * max(1.0, np.max(np.abs(a)))
+    assert np.array_equal(out["0"][1]["raw"], out["1"][1]["raw"])
+
+
+@pytest.mark.gpu
+def test_conv_extractor_through_detect_entry_points(qrm, cuda):
+    """DetectionConfig(extractor="conv") routes detect_device / detect_host (all
+    three transfer modes) through the conv stack; records equal the direct call."""
+    import dataclasses
+    base = qrm.DetectionConfig()
+    cfg = dataclasses.replace(base, extractor="conv", conv_seed=SEED)
+    imgs = cuda.cat([qrm.make_corpus(base, 1000, 20), qrm.make_corpus(base, 5000, 20, embed=False)])
+    with qrm.DetectionContext(base) as ctx:
+        _, rec0 = ctx.hidden_detect_device(imgs, weight_seed=SEED, first_draw=5, logits=False)
+        ref = qrm.records_from_device(rec0)
+    host = imgs.cpu().numpy()
+    with qrm.DetectionContext(cfg) as ctx:
+        dev = qrm.records_from_device(ctx.detect_device(imgs, first_draw=5))
+        assert np.array_equal(dev, ref)
+        for mode in (0, 1, 2):
+            out, st = ctx.detect_host(host, 5, plan=([1, 2, 1], [16, 16, 16]), mode=mode)
+            assert np.array_equal(out, ref), mode
+    with pytest.raises(qrm.InvalidInput):
+        qrm.DetectionContext(dataclasses.replace(base, extractor="cnn"))
