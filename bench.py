@@ -150,7 +150,7 @@ def run_reference_arm(args):
 HIDDEN_FLOP_PER_TILE = 2 * 64 * 64 * (27 * 64 + 7 * 576 * 64 + 576 * 60) + 2 * 60 * 60
 
 
-def hidden_submetric(ctx, pool, world, max_over_ranks, stream, batch=BATCH, reps=5):
+def hidden_submetric(ctx, pool, world, max_over_ranks, stream, batch=BATCH, reps=5, host_pool=None):
     """Learned conv extractor on one device-resident batch: tiles/s and tensor-pipe fraction."""
     import torch
 
@@ -172,7 +172,34 @@ def hidden_submetric(ctx, pool, world, max_over_ranks, stream, batch=BATCH, reps
     torch.cuda.synchronize()
     ms = max_over_ranks(a.elapsed_time(b) / reps)
     tflops = HIDDEN_FLOP_PER_TILE * batch / (ms / 1e3) / 1e12
-    return {"tiles_per_s": world * batch / (ms / 1e3), "ms_per_batch": ms, "batch": batch,
+    e2e = None
+    if host_pool is not None:
+        # end to end through the public host API with the conv extractor selected
+        # (DetectionConfig.extractor = "conv"): pinned host images -> host records
+        import dataclasses
+        import numpy as np
+        import paper_2509_02447_b200 as q
+        cfg = dataclasses.replace(ctx.cfg, extractor="conv")
+        recs_pin = torch.empty((batch, q.RECORD_DTYPE.itemsize), dtype=torch.uint8, pin_memory=True)
+        recs = recs_pin.numpy().view(q.RECORD_DTYPE).reshape(-1)
+        plan = ([1, 1, 1], [batch // 2] * 3)
+        H, W = host_pool.shape[1], host_pool.shape[2]
+        with q.DetectionContext(cfg, device=ctx.device) as cctx:
+            def one(i):
+                b0 = (i % (host_pool.shape[0] // batch)) * batch
+                _, st = cctx.detect_host(None, i * batch, plan=plan, mode=0, out=recs,
+                                         ptr=host_pool[b0].data_ptr(), shape=(batch, H, W))
+                return st
+            one(0)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            n = 3
+            for i in range(n):
+                st = one(1 + i)
+            dt = max_over_ranks(time.perf_counter() - t0)
+        e2e = {"value": world * batch * n / dt, "unit": "images/s", "h2d_bytes_per_step": int(st["h2d_bytes"]),
+               "d2h_bytes_per_step": int(st["d2h_bytes"]), "path": "qrm_detect_host mode 0, extractor=conv"}
+    return {"tiles_per_s": world * batch / (ms / 1e3), "ms_per_batch": ms, "batch": batch, "e2e": e2e,
             "arch": "9 x (conv3x3 + BN + ReLU) 64ch @ 64x64, avgpool, linear 60x60, RS gf16-15-12",
             "flop_per_tile": HIDDEN_FLOP_PER_TILE,
             "roofline": {"bound": "tensor", "achieved": tflops, "peak": peak, "unit": "TFLOP/s",
@@ -336,7 +363,7 @@ def main():
     # tcgen05 kind::f16 + pool + head + RS, same 4096-image batches.
     hidden = None
     try:
-        hidden = hidden_submetric(ctx, pool, world, max_over_ranks, stream)
+        hidden = hidden_submetric(ctx, pool, world, max_over_ranks, stream, host_pool=host_pool)
     except Exception as exc:
         hidden = {"unavailable": str(exc)}
 

@@ -1030,6 +1030,7 @@ qrm_status hidden_run(qrm_ctx* c, Workspace& W, const WindowSource& src, int64_t
             lp.act_out = lp.last ? nullptr : H.act[j & 1];
             lp.pool_out = lp.last ? H.pool : nullptr;
             lp.tiles = n;
+            if (const char* e = getenv("QRM_HIDDEN_DBG")) lp.dbg = atoi(e);  // timing experiments only
             QRM_LAUNCH(conv64_layer(H.tmap[(j - 1) & 1], H.tmap_st[j & 1], lp, c->sms, st));
         }
         HeadParams hp{};

@@ -42,7 +42,7 @@ constexpr int kHBlocks = kHPix / kHM;      // 32 blocks per tile
 constexpr int kHWBytes = 9 * kHC * kHC * 2;  // 73,728 B of bf16 weights per layer
 constexpr int kHABytes = 4 * kHSide * kHC * 2;  // 32 KB: 4 input rows
 constexpr int kHAStages = 4;
-constexpr int kHThreads = 192;             // warp 0 TMA, warp 1 MMA, warps 2-5 epilogue
+constexpr int kHThreads = 320;             // warp 0 TMA, warp 1 MMA, warps 2-9 epilogue
 constexpr int kHAcc = 4;                   // TMEM accumulator buffers (64 columns each)
 
 struct HiddenSmem {
@@ -58,69 +58,85 @@ constexpr int kHOBytes = 4 * 32 * kHC * 2;  // 16 KB: output staging, 4 KB per e
 constexpr size_t kHSmemBytes = 1024 + kHWBytes + kHAStages * kHABytes + kHOBytes + 128 + sizeof(HiddenSmem);
 static_assert(kHSmemBytes <= 232448, "conv64 shared memory exceeds 227 KB");
 
-// Epilogue of one 128-pixel block (32 pixels per warp, one per lane): bias +
-// ReLU, then either bf16 NHWC rows -> 128B-swizzled per-warp slab -> one TMA
-// store, or (last layer) the block's per-channel sums for the average pool.
+// Epilogue of one 128-pixel block. Eight epilogue warps: warp w reads TMEM
+// lane quarter q = w % 4 (32 pixels, one per lane) and channel half h (32 of the
+// 64 accumulator columns), so a block's 32 KB of TMEM is drained by twice as
+// many warps. Bias + ReLU, then either bf16 NHWC rows -> the quarter's 128B-
+// swizzled 4 KB slab (each half writes its four 16-B chunks of every row) ->
+// one TMA store per quarter, or (last layer) the block's per-channel sums for
+// the average pool. Named barriers 1..4 pair the two warps of a quarter.
+constexpr int kHEpiWarps = 8;
+constexpr int kHCh = kHC / 2;  // channels per epilogue warp
+
+__device__ __forceinline__ void quarter_sync(int q) {
+    asm volatile("bar.sync %0, 64;" ::"r"(1 + q) : "memory");
+}
+
 __device__ __forceinline__ void conv_epilogue(const HiddenLayerParams& p, const CUtensorMap* tmap_out,
-                                              const uint32_t (&acc)[kHC], const float* s_bias, float (*pool)[kHC],
-                                              uint32_t o_s, int q, int lane, int64_t tile, int blk) {
+                                              const uint32_t (&acc)[kHCh], const float* s_bias, float (*pool)[kHC],
+                                              uint32_t o_s, int q, int h, int lane, int64_t tile, int blk) {
     const int pix = blk * kHM + q * 32 + lane;
-    float v[kHC];
+    float v[kHCh];
 #pragma unroll
-    for (int c = 0; c < kHC; ++c) v[c] = fmaxf(__uint_as_float(acc[c]) + s_bias[c], 0.0f);
+    for (int c = 0; c < kHCh; ++c) v[c] = fmaxf(__uint_as_float(acc[c]) + s_bias[h * kHCh + c], 0.0f);
     if (!p.last) {
-        // Stage this warp's 32 pixels x 128 B as a 128B-swizzled slab (16-B
-        // chunk c of row r at chunk c ^ (r & 7): conflict free), then one TMA
-        // store writes the 4 KB contiguous NHWC run.
+        // 16-B chunk c of row r at chunk c ^ (r & 7): conflict-free STS.128
         const uint32_t slab = o_s + q * 4096;
-        if (lane == 0) bulk_wait_read<0>();  // previous store has read the slab
-        __syncwarp();
+        if (h == 0 && lane == 0) bulk_wait_read<0>();  // the quarter's previous store has read the slab
+        quarter_sync(q);
         const uint32_t row = slab + lane * 128;
 #pragma unroll
-        for (int c = 0; c < kHC; c += 8) {
-            uint4 o;
+        for (int c = 0; c < kHCh; c += 8) {
             __nv_bfloat162 h0 = __floats2bfloat162_rn(v[c], v[c + 1]);
             __nv_bfloat162 h1 = __floats2bfloat162_rn(v[c + 2], v[c + 3]);
             __nv_bfloat162 h2 = __floats2bfloat162_rn(v[c + 4], v[c + 5]);
             __nv_bfloat162 h3 = __floats2bfloat162_rn(v[c + 6], v[c + 7]);
-            o.x = *reinterpret_cast<uint32_t*>(&h0);
-            o.y = *reinterpret_cast<uint32_t*>(&h1);
-            o.z = *reinterpret_cast<uint32_t*>(&h2);
-            o.w = *reinterpret_cast<uint32_t*>(&h3);
-            st_shared_v4(row + ((((c >> 3) ^ lane) & 7) << 4), o);
+            const int chunk = h * 4 + (c >> 3);
+            st_shared_v4(row + (((chunk ^ lane) & 7) << 4),
+                         make_uint4(*reinterpret_cast<uint32_t*>(&h0), *reinterpret_cast<uint32_t*>(&h1),
+                                    *reinterpret_cast<uint32_t*>(&h2), *reinterpret_cast<uint32_t*>(&h3)));
         }
         fence_proxy_async_smem();
-        __syncwarp();
-        if (lane == 0) {
+        quarter_sync(q);
+        if (h == 0 && lane == 0) {
             tma_store_2d(tmap_out, slab, 0, static_cast<int>(tile * kHPix + pix - lane));
             bulk_commit();
         }
     } else {
         // Average pool, part 1: channel sums over this warp's 32 pixels by
-        // recursive halving (each step a lane keeps half the channels).
+        // recursive halving; step o keeps the upper half iff lane bit o is set,
+        // so lane L ends with channel h*32 + L.
 #pragma unroll
-        for (int o = 16, n = kHC / 2; o >= 1; o >>= 1, n >>= 1) {
+        for (int o = 16; o >= 1; o >>= 1) {
             const bool upper = (lane & o) != 0;
 #pragma unroll
-            for (int c = 0; c < n; ++c) {
-                const float send = upper ? v[c] : v[c + n];
-                const float keep = upper ? v[c + n] : v[c];
+            for (int c = 0; c < o; ++c) {
+                const float send = upper ? v[c] : v[c + o];
+                const float keep = upper ? v[c + o] : v[c];
                 v[c] = keep + __shfl_xor_sync(0xffffffffu, send, o);
             }
         }
-        // Step o kept the upper half iff lane bit log2(o) is set, adding
-        // 2*o to the channel base: lane L now holds channels 2L, 2L+1.
-        pool[q][2 * lane] = v[0];
-        pool[q][2 * lane + 1] = v[1];
-        asm volatile("bar.sync 1, 128;" ::: "memory");
-        if (q == 0 && lane < kHC / 2) {
-            // part 2: fixed-order sum of the 4 warps -> per-block partial
-            for (int c2 = lane * 2; c2 < lane * 2 + 2; ++c2)
-                p.pool_out[(tile * kHBlocks + blk) * kHC + c2] =
-                    ((pool[0][c2] + pool[1][c2]) + pool[2][c2]) + pool[3][c2];
+        pool[q][h * kHCh + lane] = v[0];
+        asm volatile("bar.sync 5, 256;" ::: "memory");
+        if (q == 0) {
+            // part 2: fixed-order sum of the 4 quarters -> per-block partial
+            const int c2 = h * kHCh + lane;
+            p.pool_out[(tile * kHBlocks + blk) * kHC + c2] = ((pool[0][c2] + pool[1][c2]) + pool[2][c2]) + pool[3][c2];
         }
-        asm volatile("bar.sync 1, 128;" ::: "memory");
+        asm volatile("bar.sync 5, 256;" ::: "memory");
     }
+}
+
+// This warp's 32 accumulator columns of TMEM buffer `a` (lane quarter q).
+__device__ __forceinline__ void load_acc_half(uint32_t tmem, int q, int h, int a, uint32_t (&acc)[kHCh]) {
+#pragma unroll
+    for (int c = 0; c < kHCh / 16; ++c) {
+        uint32_t r16[16];
+        tmem_ld16(tmem + (static_cast<uint32_t>(q * 32) << 16) + a * kHC + h * kHCh + c * 16, r16);
+#pragma unroll
+        for (int j = 0; j < 16; ++j) acc[c * 16 + j] = r16[j];
+    }
+    tmem_ld_wait();
 }
 
 __global__ void __launch_bounds__(kHThreads, 1)
@@ -146,7 +162,7 @@ __global__ void __launch_bounds__(kHThreads, 1)
         }
         for (int a = 0; a < kHAcc; ++a) {
             mbar_init(&sm.acc_full[a], 1);
-            mbar_init(&sm.acc_empty[a], 4);
+            mbar_init(&sm.acc_empty[a], kHEpiWarps);
         }
         mbar_fence_init();
     }
@@ -213,27 +229,22 @@ __global__ void __launch_bounds__(kHThreads, 1)
         }
     } else {
         // ----------------------------------------------------- epilogue ----
-        const int q = warp & 3;  // TMEM lane quarter this warp may access
+        const int q = warp & 3, h = (warp - 2) >> 2;  // TMEM lane quarter, channel half
         int i = 0;
         for (int64_t b = blockIdx.x; b < nblocks; b += gridDim.x, ++i) {
             const int a = i % kHAcc;
             mbar_wait(&sm.acc_full[a], (i / kHAcc) & 1);
             tc_fence_after();
-            uint32_t acc[kHC];
-#pragma unroll
-            for (int c = 0; c < kHC / 16; ++c) {
-                uint32_t r16[16];
-                tmem_ld16(tmem + (static_cast<uint32_t>(q * 32) << 16) + a * kHC + c * 16, r16);
-#pragma unroll
-                for (int j = 0; j < 16; ++j) acc[c * 16 + j] = r16[j];
-            }
-            tmem_ld_wait();
+            uint32_t acc[kHCh];
+            load_acc_half(tmem, q, h, a, acc);
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&sm.acc_empty[a]);
-            conv_epilogue(p, &tmap_out, acc, s_bias, sm.pool, o_s, q, lane, b / kHBlocks, static_cast<int>(b % kHBlocks));
+            if (!(p.dbg & 16))  // timing experiment: skip the epilogue math/stores
+                conv_epilogue(p, &tmap_out, acc, s_bias, sm.pool, o_s, q, h, lane, b / kHBlocks,
+                              static_cast<int>(b % kHBlocks));
         }
-        if (!p.last && lane == 0) bulk_wait<0>();
+        if (!p.last && h == 0 && lane == 0) bulk_wait<0>();
     }
     __syncthreads();
     if (warp == 1) {
@@ -254,7 +265,7 @@ __global__ void __launch_bounds__(kHThreads, 1)
 //   full[s]     (even CTA)  2 arrivals (+tx): both CTAs' TMA windows landed
 //   empty[s]    (each CTA)  multicast commit of the pair's MMAs
 //   acc_full[a] (each CTA)  multicast commit
-//   acc_empty[a](even CTA)  8 arrivals: the 4 epilogue warps of both CTAs
+//   acc_empty[a](even CTA)  16 arrivals: the 8 epilogue warps of both CTAs
 constexpr int kPWBytes = kHWBytes / 2;  // 36 KB: 9 taps x 32 co x 64 ci
 constexpr int kPAStages = 5;
 struct PairSmem {
@@ -293,7 +304,7 @@ __global__ void __launch_bounds__(kHThreads, 1)
         }
         for (int a = 0; a < kHAcc; ++a) {
             mbar_init(&sm.acc_full[a], 1);
-            mbar_init(&sm.acc_empty[a], 8);
+            mbar_init(&sm.acc_empty[a], 2 * kHEpiWarps);
         }
         mbar_fence_init();
     }
@@ -362,7 +373,7 @@ __global__ void __launch_bounds__(kHThreads, 1)
     } else {
         // ----------------------------------------------------- epilogue ----
         cluster_sync_all();
-        const int q = warp & 3;
+        const int q = warp & 3, h = (warp - 2) >> 2;
         uint32_t empty0[kHAcc];
 #pragma unroll
         for (int a = 0; a < kHAcc; ++a) empty0[a] = map_to_rank(smem_u32(&sm.acc_empty[a]), 0);
@@ -371,22 +382,16 @@ __global__ void __launch_bounds__(kHThreads, 1)
             const int a = i % kHAcc;
             mbar_wait(&sm.acc_full[a], (i / kHAcc) & 1);
             tc_fence_after();
-            uint32_t acc[kHC];
-#pragma unroll
-            for (int c = 0; c < kHC / 16; ++c) {
-                uint32_t r16[16];
-                tmem_ld16(tmem + (static_cast<uint32_t>(q * 32) << 16) + a * kHC + c * 16, r16);
-#pragma unroll
-                for (int j = 0; j < 16; ++j) acc[c * 16 + j] = r16[j];
-            }
-            tmem_ld_wait();
+            uint32_t acc[kHCh];
+            load_acc_half(tmem, q, h, a, acc);
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive_cluster(empty0[a]);
-            conv_epilogue(p, &tmap_out, acc, s_bias, sm.pool, o_s, q, lane, b / kPairBlocks,
+            if (!(p.dbg & 16))
+            conv_epilogue(p, &tmap_out, acc, s_bias, sm.pool, o_s, q, h, lane, b / kPairBlocks,
                           static_cast<int>(b % kPairBlocks) * 2 + static_cast<int>(rank));
         }
-        if (!p.last && lane == 0) bulk_wait<0>();
+        if (!p.last && h == 0 && lane == 0) bulk_wait<0>();
     }
     __syncwarp();
     if (warp == 0) cluster_wait();  // the TMA warp's wait of barrier phase 2
