@@ -17,6 +17,7 @@
 
 #include <array>
 #include <cstdint>
+#include <filesystem>
 #include <functional>
 #include <mutex>
 #include <optional>
@@ -194,6 +195,8 @@ ImageBuffer denormalize(const ImageBuffer& img);  // host (input generation)
 ImageBuffer resize_bilinear(const ImageBuffer& img, int out_w, int out_h);  // GPU
 ImageBuffer center_crop(const ImageBuffer& img, int side_w, int side_h);    // GPU (byte) / copy (normalized)
 ImageBuffer synthetic_image(uint64_t seed, int w, int h);                   // GPU corpus generator
+ImageBuffer read_ppm(const std::filesystem::path& path);                     // host (qrm_ppm_read)
+void write_ppm(const ImageBuffer& img, const std::filesystem::path& path);   // host (qrm_ppm_write)
 
 // --------------------------------------------------------- transforms.hpp
 inline constexpr int kWorkingSize = 256;
@@ -364,6 +367,8 @@ class CorrectionCache {
 public:
     explicit CorrectionCache(const CacheConfig& cfg) : cfg_(cfg) {}
     std::pair<std::optional<DecodeResult>, bool> correct(const BitVec& raw, const CodeParams& params);
+    // correct()'s bookkeeping for a word decoded elsewhere (the GPU): returns the hit flag.
+    bool record(const BitVec& raw, const std::optional<DecodeResult>& decoded);
     size_t size() const;
     uint64_t hits() const { return hits_; }
     uint64_t lookups() const { return lookups_; }

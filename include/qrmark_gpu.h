@@ -170,6 +170,38 @@ QRM_EXPORT qrm_status qrm_hidden_detect_device(qrm_ctx* ctx, const uint8_t* imag
 #define QRM_EXTRACTOR_CONV 1
 QRM_EXPORT qrm_status qrm_ctx_set_extractor(qrm_ctx* ctx, int kind, uint64_t weight_seed);
 
+/* ---- formats either side of the path (ingest and report) ---------------- */
+
+/* read_ppm (image.cpp:129-146): P6, maxval 255, '#' comments, the reference's
+ * InvalidInput messages. dst == NULL: header only (w, h). Else the raster
+ * (w*h*3 bytes, HWC) goes to dst, which must hold cap >= w*h*3 bytes. */
+QRM_EXPORT qrm_status qrm_ppm_read(const char* path, uint8_t* dst, int64_t cap, int* w, int* h);
+/* write_ppm (image.cpp:148-156). */
+QRM_EXPORT qrm_status qrm_ppm_write(const char* path, const uint8_t* img, int w, int h);
+/* ingest (cli.cpp:22-45) of `count` same-size P6 files, decoded in parallel by
+ * `threads` host threads straight into dst + i*image_stride (typically pinned
+ * memory that qrm_detect_host then transfers). status[i] (nullable) per file;
+ * returns the first failure. */
+QRM_EXPORT qrm_status qrm_ppm_read_batch(const char* const* paths, int64_t count, int w, int h, uint8_t* dst,
+                                         int64_t image_stride, int threads, int32_t* status);
+/* DetectionRecord::cache_hit: the CorrectionCache policy (detect.cpp:86-128;
+ * capacity / stale_after of CacheConfig, detect.hpp:19-23) replayed over the
+ * records' raw words in index order (the reference with one correct worker).
+ * The GPU decoders are O(1) per word, so the codebook is never consulted for
+ * speed; this reproduces the flag the reference reports. hit: count bytes. */
+QRM_EXPORT qrm_status qrm_cache_hits(const qrm_record* records, int64_t count, int64_t capacity,
+                                     uint64_t stale_after, uint8_t* hit);
+/* The "records" array of cmd_detect's report (cli.cpp:279-281): record_to_json
+ * (json_io.cpp:98-120, deterministic stage times) of every record, in
+ * nlohmann::json dump(2) layout. Index of record i = first_index + i.
+ * cache_hit replays CorrectionCache (detect.cpp:86-128; CacheConfig
+ * detect.hpp:19-23: enabled, capacity, stale_after) over the records in index
+ * order. Writes at most cap-1 bytes + NUL to out (nullable); *len = the full
+ * length. */
+QRM_EXPORT qrm_status qrm_records_json(const qrm_record* records, int64_t count, int n_bits, int k_bits,
+                                       int64_t first_index, int cache_enabled, int64_t cache_capacity,
+                                       uint64_t stale_after, char* out, int64_t cap, int64_t* len);
+
 /* preprocess (transforms.cpp:42-47) of one host image -> 256*256*3 floats. */
 QRM_EXPORT qrm_status qrm_preprocess_host(const uint8_t* image, int w, int h, float* out);
 

@@ -400,6 +400,11 @@ class Reference(_Common):
         L.ref_detect_sequential.argtypes = [C.POINTER(C.POINTER(C.c_uint8)), C.POINTER(C.c_int),
                                             C.POINTER(C.c_int), C.c_int64, C.c_uint64, C.POINTER(_RefCfg),
                                             C.POINTER(_RefRecords)]
+        L.ref_read_ppm.argtypes = [C.c_char_p, C.POINTER(C.c_uint8), C.c_int64, C.POINTER(C.c_int), C.POINTER(C.c_int)]
+        L.ref_write_ppm.argtypes = [C.c_char_p, C.POINTER(C.c_uint8), C.c_int, C.c_int]
+        L.ref_detect_json.restype = C.c_int64
+        L.ref_detect_json.argtypes = [C.POINTER(C.POINTER(C.c_uint8)), C.POINTER(C.c_int), C.POINTER(C.c_int),
+                                      C.c_int64, C.POINTER(_RefCfg), C.c_char_p, C.c_int64]
         L.ref_detect_batch.restype = C.c_int64
         L.ref_detect_batch.argtypes = [C.POINTER(C.POINTER(C.c_uint8)), C.POINTER(C.c_int), C.POINTER(C.c_int),
                                        C.c_int64, C.POINTER(_RefCfg), C.POINTER(C.c_int), C.POINTER(C.c_int),
@@ -515,11 +520,11 @@ class Reference(_Common):
         self.lib.ref_pattern(key_seed, n_bits, l, bit, _p(out, C.c_int8))
         return out
 
-    def _cfg(self, cfg: DetectCfg, rs_workers=32, cache=True):
+    def _cfg(self, cfg: DetectCfg, rs_workers=32, cache=True, cache_capacity=4096, stale_after=1 << 20):
         m, n, k, _ = cfg.code
         msg = self._msg(cfg)
         c = _RefCfg(m, n, k, cfg.tile_size, STRATEGY[cfg.strategy], cfg.tile_seed, cfg.key_seed, cfg.alpha,
-                    _u8p(msg), rs_workers, cfg.fpr, int(cache), 4096, 1 << 20)
+                    _u8p(msg), rs_workers, cfg.fpr, int(cache), cache_capacity, stale_after)
         return c, msg
 
     def _records(self, count, cfg: DetectCfg):
@@ -548,6 +553,36 @@ class Reference(_Common):
         if self.lib.ref_detect_sequential(ptrs, ws, hs, len(keep), first_draw, C.byref(c), C.byref(r)):
             raise ValueError(self.last_error())
         return arrs
+
+    def read_ppm(self, path):
+        """read_ppm (image.cpp:129-146) -> uint8 [H, W, 3]; ValueError carries the reference's message."""
+        w, h = C.c_int(), C.c_int()
+        p = os.fsencode(path)
+        if self.lib.ref_read_ppm(p, None, 0, C.byref(w), C.byref(h)):
+            raise ValueError(self.last_error())
+        out = np.empty((h.value, w.value, 3), np.uint8)
+        if self.lib.ref_read_ppm(p, _u8p(out), out.nbytes, C.byref(w), C.byref(h)):
+            raise ValueError(self.last_error())
+        return out
+
+    def write_ppm(self, img, path):
+        img = np.ascontiguousarray(img, np.uint8)
+        if self.lib.ref_write_ppm(os.fsencode(path), _u8p(img), img.shape[1], img.shape[0]):
+            raise ValueError(self.last_error())
+
+    def detect_json(self, images, cfg: DetectCfg = DetectCfg(), rs_workers: int = 1, cache: bool = True,
+                    cache_capacity: int = 4096, stale_after: int = 1 << 20) -> str:
+        """cmd_detect's records array: detect_batch + record_to_json(deterministic) + dump(2).
+        rs_workers = 1 makes the codebook's hit order deterministic (index order)."""
+        keep, ptrs, ws, hs = self._imgs(images)
+        c, msg = self._cfg(cfg, rs_workers=rs_workers, cache=cache, cache_capacity=cache_capacity,
+                           stale_after=stale_after)
+        n = self.lib.ref_detect_json(ptrs, ws, hs, len(keep), C.byref(c), None, 0)
+        if n < 0:
+            raise ValueError(self.last_error())
+        buf = C.create_string_buffer(n + 1)
+        self.lib.ref_detect_json(ptrs, ws, hs, len(keep), C.byref(c), buf, n + 1)
+        return buf.value.decode()
 
     def detect_batch(self, images, cfg: DetectCfg = DetectCfg(), plan=None, rs_workers=32, records=True):
         """detect_batch (detect.cpp:250) -> (records or None, wall_ns)."""

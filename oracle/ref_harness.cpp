@@ -1,7 +1,7 @@
 // C-ABI shim over the UNMODIFIED reference library (TEST INFRASTRUCTURE ONLY).
 //
 // Compiled together with /root/reference/proj/src/{gf,rs,image,transforms,tiling,
-// stego,sched,detect,sim}.cpp by oracle/Makefile into oracle/_ref/libqrmark_ref.so.
+// stego,sched,detect,sim,json_io}.cpp by oracle/Makefile into oracle/_ref/libqrmark_ref.so.
 // Every entry point calls the reference's own public API; nothing here
 // re-implements reference arithmetic except `default_message`, which lives in
 // cli.cpp (not compiled: it needs CLI11) and is restated from cli.cpp:47-51.
@@ -22,6 +22,7 @@
 #include "qrmark/detect.hpp"
 #include "qrmark/gf.hpp"
 #include "qrmark/image.hpp"
+#include "qrmark/json_io.hpp"
 #include "qrmark/rng.hpp"
 #include "qrmark/rs.hpp"
 #include "qrmark/sched.hpp"
@@ -429,6 +430,52 @@ REF_API int64_t ref_detect_batch(const uint8_t* const* imgs, const int* ws, cons
         wall = rep.wall_ns;
     });
     return wall;
+}
+
+
+// read_ppm (image.cpp:129-146). dst == nullptr: header only.
+REF_API int ref_read_ppm(const char* path, uint8_t* dst, int64_t cap, int* w, int* h) {
+    return guarded([&] {
+        ImageBuffer img = read_ppm(path);
+        *w = img.width;
+        *h = img.height;
+        if (dst) {
+            if (cap < static_cast<int64_t>(img.bytes.size())) throw InvalidInput("harness: buffer too small");
+            std::memcpy(dst, img.bytes.data(), img.bytes.size());
+        }
+    });
+}
+
+// write_ppm (image.cpp:148-156).
+REF_API int ref_write_ppm(const char* path, const uint8_t* img, int w, int h) {
+    return guarded([&] {
+        ImageBuffer b = ImageBuffer::make_byte(w, h);
+        std::memcpy(b.bytes.data(), img, b.bytes.size());
+        write_ppm(b, path);
+    });
+}
+
+// cmd_detect's "records" (cli.cpp:234, 279-281): detect_batch over the images,
+// then json::array of record_to_json(rec, deterministic = true), dump(2).
+// Returns the length; copies at most cap-1 bytes + NUL into out.
+REF_API int64_t ref_detect_json(const uint8_t* const* imgs, const int* ws, const int* hs, int64_t count,
+                                const ref_detect_cfg* c, char* out, int64_t cap) {
+    int64_t len = -1;
+    guarded([&] {
+        DetectionConfig cfg = config_of(c);
+        std::vector<ImageBuffer> images = images_of(imgs, ws, hs, count);
+        auto recs = detect_batch(images, cfg);
+        nlohmann::json arr = nlohmann::json::array();
+        for (const auto& r : recs) arr.push_back(record_to_json(r, true));
+        const std::string s = arr.dump(2);
+        len = static_cast<int64_t>(s.size());
+        if (out && cap > 0) {
+            const int64_t n = std::min<int64_t>(cap - 1, len);
+            std::memcpy(out, s.data(), static_cast<size_t>(n));
+            out[n] = '\0';
+        }
+    });
+    return len;
 }
 
 // allocate_streams (sched.cpp:50). Returns the error code (0 ok).

@@ -27,7 +27,7 @@ LIB_PATH = os.path.join(_HERE, "_lib", "libqrmark_b200.so")
 # Exported symbols of include/qrmark_gpu.h (checked by the CPU test suite).
 ABI_SYMBOLS = (
     "qrm_last_error", "qrm_abi_version", "qrm_device_count", "qrm_ctx_create", "qrm_ctx_destroy", "qrm_ctx_info",
-    "qrm_ctx_set_extractor",
+    "qrm_ctx_set_extractor", "qrm_ppm_read", "qrm_ppm_write", "qrm_ppm_read_batch", "qrm_records_json", "qrm_cache_hits",
     "qrm_detect_device", "qrm_detect_host", "qrm_detect_ragged", "qrm_extract_device", "qrm_preprocess_host",
     "qrm_rs_decode_packed_device", "qrm_rs_decode_symbols_device", "qrm_rs_stress_device", "qrm_rs_encode_packed",
     "qrm_verify_threshold", "qrm_make_corpus_device", "qrm_patterns_device", "qrm_allocate_streams",
@@ -98,6 +98,10 @@ def lib() -> C.CDLL:
         L.qrm_ctx_destroy.argtypes = [vp]
         L.qrm_ctx_info.argtypes = [vp, C.POINTER(u64), C.POINTER(u64), C.POINTER(i32), C.POINTER(i32)]
         L.qrm_ctx_set_extractor.argtypes = [vp, i32, u64]
+        L.qrm_ppm_read.argtypes = [C.c_char_p, vp, i64, C.POINTER(i32), C.POINTER(i32)]
+        L.qrm_ppm_write.argtypes = [C.c_char_p, vp, i32, i32]
+        L.qrm_ppm_read_batch.argtypes = [C.POINTER(C.c_char_p), i64, i32, i32, vp, i64, i32, vp]
+        L.qrm_records_json.argtypes = [vp, i64, i32, i32, i64, i32, i64, u64, vp, i64, C.POINTER(i64)]
         L.qrm_detect_device.argtypes = [vp, vp, i64, i32, i32, i64, u64, vp, vp]
         L.qrm_detect_host.argtypes = [vp, vp, i64, i32, i32, i64, u64, vp, C.POINTER(_Plan), i32,
                                       C.POINTER(_HostStats)]
@@ -528,6 +532,53 @@ def semantic_fields(rec: np.ndarray, code: CodeParams) -> dict:
             "msg": np.where(rec["status"] == 1, rec["msg"], 0).astype(np.uint64),
             "errors": rec["errors"].astype(np.int32), "bit_acc": rec["matches"] / float(nb),
             "verified": rec["verified"].astype(bool)}
+
+
+# --------------------------------------------------------------- formats --
+def read_ppm(path) -> np.ndarray:
+    """read_ppm (image.cpp:129-146) -> uint8 [H, W, 3]."""
+    w, h = C.c_int(), C.c_int()
+    p = os.fsencode(path)
+    _check(lib().qrm_ppm_read(p, None, 0, C.byref(w), C.byref(h)))
+    out = np.empty((h.value, w.value, 3), np.uint8)
+    _check(lib().qrm_ppm_read(p, out.ctypes.data, out.nbytes, C.byref(w), C.byref(h)))
+    return out
+
+
+def write_ppm(img: np.ndarray, path) -> None:
+    """write_ppm (image.cpp:148-156)."""
+    img = np.ascontiguousarray(img, np.uint8)
+    _check(lib().qrm_ppm_write(os.fsencode(path), img.ctypes.data, img.shape[1], img.shape[0]))
+
+
+def read_ppm_batch(paths, out=None, threads: int = 0):
+    """ingest (cli.cpp:22-45) of same-size P6 files, decoded in parallel straight
+    into `out` (uint8 [N, H, W, 3]; numpy or a pinned torch tensor)."""
+    paths = [os.fsencode(p) for p in paths]
+    w, h = C.c_int(), C.c_int()
+    _check(lib().qrm_ppm_read(paths[0], None, 0, C.byref(w), C.byref(h)))
+    if out is None:
+        out = np.empty((len(paths), h.value, w.value, 3), np.uint8)
+    arr = (C.c_char_p * len(paths))(*paths)
+    _check(lib().qrm_ppm_read_batch(arr, len(paths), w.value, h.value, _ptr(out), h.value * w.value * 3,
+                                    threads or (os.cpu_count() or 1), None))
+    return out
+
+
+def records_json(rec: np.ndarray, code: CodeParams, first_index: int = 0, cache=(True, 4096, 1 << 20)) -> str:
+    """The "records" array of cmd_detect's report (cli.cpp:279-281), record_to_json
+    (json_io.cpp:98-120) per record in nlohmann dump(2) layout; cache_hit from the
+    CorrectionCache policy (enabled, capacity, stale_after) in index order."""
+    rec = np.ascontiguousarray(rec)
+    n = C.c_int64()
+    nb, kb = code.codeword_bits(), code.message_bits()
+    en, capy, stale = int(cache[0]), int(cache[1]), int(cache[2])
+    _check(lib().qrm_records_json(rec.ctypes.data, len(rec), nb, kb, first_index, en, capy, stale, None, 0,
+                                  C.byref(n)))
+    buf = C.create_string_buffer(n.value + 1)
+    _check(lib().qrm_records_json(rec.ctypes.data, len(rec), nb, kb, first_index, en, capy, stale, buf,
+                                  n.value + 1, C.byref(n)))
+    return buf.value.decode()
 
 
 # ------------------------------------------------------------- scheduler --

@@ -67,6 +67,13 @@ qrm_status fail(qrm_status s, const std::string& msg) {
     return s;
 }
 
+}  // namespace
+
+// Shared with the other host translation units (formats.cpp).
+qrm_status qrm::report_error(qrm_status s, const std::string& msg) { return fail(s, msg); }
+
+namespace {
+
 #define QRM_CUDA(call)                                                                          \
     do {                                                                                        \
         cudaError_t e_ = (call);                                                                \

@@ -648,10 +648,33 @@ bool verify(const BitVec& a, const BitVec& b, double fpr) {
     return k >= verify_threshold(static_cast<int>(a.size()), fpr);
 }
 
-std::pair<std::optional<DecodeResult>, bool> CorrectionCache::correct(const BitVec& raw, const CodeParams& params) {
+static std::string cache_key(const BitVec& raw) {
     std::string key((raw.size() + 7) / 8, '\0');  // LSB-first bit packing (detect.cpp:77-82)
     for (size_t i = 0; i < raw.size(); ++i)
         if (raw[i]) key[i / 8] |= static_cast<char>(1 << (i % 8));
+    return key;
+}
+bool CorrectionCache::record(const BitVec& raw, const std::optional<DecodeResult>& decoded) {
+    // correct()'s bookkeeping with the decode already done on the GPU
+    std::string key = cache_key(raw);
+    std::lock_guard<std::mutex> lk(mu_);
+    ++tick_;
+    ++lookups_;
+    evict_locked();
+    auto it = map_.find(key);
+    if (it != map_.end()) {
+        ++hits_;
+        it->second.last_access = tick_;
+        return true;
+    }
+    auto [jt, ins] = map_.try_emplace(std::move(key));
+    jt->second.result = decoded;
+    jt->second.last_access = tick_;
+    evict_locked();
+    return false;
+}
+std::pair<std::optional<DecodeResult>, bool> CorrectionCache::correct(const BitVec& raw, const CodeParams& params) {
+    std::string key = cache_key(raw);
     {
         std::lock_guard<std::mutex> lk(mu_);
         ++tick_;
@@ -687,6 +710,19 @@ void CorrectionCache::evict_locked() {
 size_t CorrectionCache::size() const {
     std::lock_guard<std::mutex> lk(mu_);
     return map_.size();
+}
+
+ImageBuffer read_ppm(const std::filesystem::path& path) {
+    int w = 0, h = 0;
+    const std::string p = path.string();
+    check(qrm_ppm_read(p.c_str(), nullptr, 0, &w, &h));
+    ImageBuffer img = ImageBuffer::make_byte(w, h);
+    check(qrm_ppm_read(p.c_str(), img.bytes.data(), static_cast<int64_t>(img.bytes.size()), &w, &h));
+    return img;
+}
+void write_ppm(const ImageBuffer& img, const std::filesystem::path& path) {
+    if (img.form != PixelForm::byte) throw InvalidInput("write_ppm expects byte form");
+    check(qrm_ppm_write(path.string().c_str(), img.bytes.data(), img.width, img.height));
 }
 
 struct GpuContext {
@@ -791,6 +827,16 @@ std::vector<DetectionRecord> DetectionContext::detect_many(std::span<const Image
         check(qrm_detect_ragged(gpu_->h, ptrs.data(), ws.data(), hs.data(), n, first_draw, rec.data()));
     }
     for (int64_t i = 0; i < n; ++i) out[i] = to_record(rec[i], first_draw + i, cfg_);
+    if (cfg_.cache.enabled) {
+        // DetectionRecord::cache_hit as the reference reports it (detect.cpp:326-333):
+        // the context's codebook sees the words in index order
+        for (int64_t i = 0; i < n; ++i) {
+            std::optional<DecodeResult> d;
+            if (out[i].corrected) d = DecodeResult{*out[i].corrected, rs_encode(*out[i].corrected, cfg_.code),
+                                                   out[i].errors_corrected};
+            out[i].cache_hit = cache_.record(out[i].raw_bits, d);
+        }
+    }
     return out;
 }
 

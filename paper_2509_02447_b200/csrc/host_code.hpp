@@ -43,4 +43,7 @@ std::vector<uint16_t> encode_symbols(int m, int n, int k, const std::vector<uint
 // verify_threshold (detect.cpp:31-66). Returns -1 for invalid arguments.
 int verify_threshold(int n_bits, double fpr);
 
+// Sets qrm_last_error() for this thread and returns s (defined in capi.cpp).
+qrm_status report_error(qrm_status s, const std::string& msg);
+
 }  // namespace qrm

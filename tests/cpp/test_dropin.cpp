@@ -311,6 +311,17 @@ static void gpu_image() {
     CHECK(syn.width == 64 && syn.height == 48 && syn.bytes.size() == 64 * 48 * 3);
 }
 
+static void host_ppm() {
+    ImageBuffer img = noise_image(12, 37, 21);
+    const std::string path = "/tmp/qrm_dropin_test.ppm";
+    write_ppm(img, path);
+    ImageBuffer back = read_ppm(path);
+    CHECK(back.width == 37 && back.height == 21 && back.bytes == img.bytes);
+    CHECK_THROWS_AS(read_ppm("/tmp/qrm_no_such_file.ppm"), InvalidInput);
+    CHECK_THROWS_AS(write_ppm(ImageBuffer::make_normalized(2, 2), path), InvalidInput);
+    std::remove(path.c_str());
+}
+
 static void gpu_stego_detect() {
     WatermarkKey key{1, 60, 0.04};
     SpreadSpectrumCodec codec(key, 64);
@@ -342,6 +353,7 @@ static void gpu_stego_detect() {
     auto rn = detect_batch(neg, cfg);
     for (size_t i = 0; i < rp.size(); ++i) {
         CHECK(rp[i].image_index == i);
+        CHECK(rp[i].cache_hit == (i > 0));  // one raw word: the codebook hits after the first (detect.cpp:326-333)
         CHECK(rp[i].verified && rp[i].corrected && *rp[i].corrected == msg && rp[i].errors_corrected == 0);
         CHECK(rp[i].bit_acc == 1.0);
         CHECK(!rn[i].verified);
@@ -415,7 +427,7 @@ int main(int argc, char** argv) {
         bool gpu;
         void (*fn)();
     } cases[] = {{"gf", false, host_gf},          {"rs_encode", false, host_rs_encode},
-                 {"tiling_sched", false, host_tiling_sched}, {"rs_gpu", true, gpu_rs},
+                 {"tiling_sched", false, host_tiling_sched}, {"ppm", false, host_ppm}, {"rs_gpu", true, gpu_rs},
                  {"image_gpu", true, gpu_image},  {"stego_detect_gpu", true, gpu_stego_detect},
                  {"conv_detect_gpu", true, gpu_conv_detect}};
     for (auto& c : cases) {
