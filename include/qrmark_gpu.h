@@ -170,6 +170,24 @@ QRM_EXPORT qrm_status qrm_hidden_detect_device(qrm_ctx* ctx, const uint8_t* imag
 #define QRM_EXTRACTOR_CONV 1
 QRM_EXPORT qrm_status qrm_ctx_set_extractor(qrm_ctx* ctx, int kind, uint64_t weight_seed);
 
+/* ---- robustness attacks -------------------------------- */
+
+/* TransformOp (transforms.hpp:22-35), in the reference's order. */
+enum {
+    QRM_ATTACK_CENTERCROP = 0, QRM_ATTACK_RESIZETO, QRM_ATTACK_NORMALIZE, QRM_ATTACK_CROP, QRM_ATTACK_RESIZE,
+    QRM_ATTACK_BRIGHTNESS, QRM_ATTACK_CONTRAST, QRM_ATTACK_SATURATION, QRM_ATTACK_SHARPNESS, QRM_ATTACK_BLUR,
+    QRM_ATTACK_OVERLAY_TEXT, QRM_ATTACK_JPEG_APPROX
+};
+/* apply_attack (transforms.cpp:289-362) on `count` same-size byte images in
+ * device memory (image i at images + i*image_stride), bit-exact with the
+ * reference. Output sizes depend on the op: out == NULL only reports them in
+ * *out_w / *out_h. Results go to out + i*out_stride (bytes; NORMALIZE writes
+ * floats). Parameter checks and messages are the reference's (InvalidInput).
+ * Stream-ordered; temporaries are freed before return. */
+QRM_EXPORT qrm_status qrm_attack_device(const uint8_t* images, int64_t count, int w, int h, int64_t image_stride,
+                                        int op, double param, void* out, int64_t out_stride, int* out_w, int* out_h,
+                                        void* stream);
+
 /* ---- formats either side of the path (ingest and report) ---------------- */
 
 /* read_ppm (image.cpp:129-146): P6, maxval 255, '#' comments, the reference's

@@ -402,6 +402,8 @@ class Reference(_Common):
                                             C.POINTER(_RefRecords)]
         L.ref_read_ppm.argtypes = [C.c_char_p, C.POINTER(C.c_uint8), C.c_int64, C.POINTER(C.c_int), C.POINTER(C.c_int)]
         L.ref_write_ppm.argtypes = [C.c_char_p, C.POINTER(C.c_uint8), C.c_int, C.c_int]
+        L.ref_apply_attack.argtypes = [C.POINTER(C.c_uint8), C.c_int, C.c_int, C.c_char_p, C.c_double, C.c_void_p,
+                                       C.c_int64, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int)]
         L.ref_detect_json.restype = C.c_int64
         L.ref_detect_json.argtypes = [C.POINTER(C.POINTER(C.c_uint8)), C.POINTER(C.c_int), C.POINTER(C.c_int),
                                       C.c_int64, C.POINTER(_RefCfg), C.c_char_p, C.c_int64]
@@ -569,6 +571,18 @@ class Reference(_Common):
         img = np.ascontiguousarray(img, np.uint8)
         if self.lib.ref_write_ppm(os.fsencode(path), _u8p(img), img.shape[1], img.shape[0]):
             raise ValueError(self.last_error())
+
+    def apply_attack(self, img, op: str, param: float):
+        """apply_attack (transforms.cpp:289-362) -> uint8 [H', W', 3] (float32 for normalize)."""
+        img = np.ascontiguousarray(img, np.uint8)
+        ow, oh, fl = C.c_int(), C.c_int(), C.c_int()
+        args = (_u8p(img), img.shape[1], img.shape[0], op.encode(), float(param))
+        if self.lib.ref_apply_attack(*args, None, 0, C.byref(ow), C.byref(oh), C.byref(fl)):
+            raise ValueError(self.last_error())
+        out = np.empty((oh.value, ow.value, 3), np.float32 if fl.value else np.uint8)
+        if self.lib.ref_apply_attack(*args, out.ctypes.data, out.nbytes, C.byref(ow), C.byref(oh), C.byref(fl)):
+            raise ValueError(self.last_error())
+        return out
 
     def detect_json(self, images, cfg: DetectCfg = DetectCfg(), rs_workers: int = 1, cache: bool = True,
                     cache_capacity: int = 4096, stale_after: int = 1 << 20) -> str:

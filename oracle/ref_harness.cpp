@@ -478,6 +478,27 @@ REF_API int64_t ref_detect_json(const uint8_t* const* imgs, const int* ws, const
     return len;
 }
 
+
+// apply_attack (transforms.cpp:289-362) via TransformSpec::parse (the CLI's
+// names). out: bytes, or floats for "normalize" (*is_float = 1).
+REF_API int ref_apply_attack(const uint8_t* img, int w, int h, const char* op, double param, void* out, int64_t cap,
+                             int* ow, int* oh, int* is_float) {
+    return guarded([&] {
+        ImageBuffer b = ImageBuffer::make_byte(w, h);
+        std::memcpy(b.bytes.data(), img, b.bytes.size());
+        ImageBuffer r = apply_attack(b, TransformSpec::parse(op, param));
+        *ow = r.width;
+        *oh = r.height;
+        *is_float = r.form == PixelForm::normalized;
+        const int64_t bytes = *is_float ? static_cast<int64_t>(r.values.size() * sizeof(float))
+                                        : static_cast<int64_t>(r.bytes.size());
+        if (out) {
+            if (cap < bytes) throw InvalidInput("harness: buffer too small");
+            std::memcpy(out, *is_float ? static_cast<const void*>(r.values.data()) : r.bytes.data(), bytes);
+        }
+    });
+}
+
 // allocate_streams (sched.cpp:50). Returns the error code (0 ok).
 REF_API int ref_allocate_streams(int stages, const double* time, const double* memory, double b0,
                                  int global_batch, int budget, double m_cap, double eps, int stall_cap,

@@ -27,7 +27,7 @@ LIB_PATH = os.path.join(_HERE, "_lib", "libqrmark_b200.so")
 # Exported symbols of include/qrmark_gpu.h (checked by the CPU test suite).
 ABI_SYMBOLS = (
     "qrm_last_error", "qrm_abi_version", "qrm_device_count", "qrm_ctx_create", "qrm_ctx_destroy", "qrm_ctx_info",
-    "qrm_ctx_set_extractor", "qrm_ppm_read", "qrm_ppm_write", "qrm_ppm_read_batch", "qrm_records_json", "qrm_cache_hits",
+    "qrm_ctx_set_extractor", "qrm_ppm_read", "qrm_ppm_write", "qrm_ppm_read_batch", "qrm_records_json", "qrm_cache_hits", "qrm_attack_device",
     "qrm_detect_device", "qrm_detect_host", "qrm_detect_ragged", "qrm_extract_device", "qrm_preprocess_host",
     "qrm_rs_decode_packed_device", "qrm_rs_decode_symbols_device", "qrm_rs_stress_device", "qrm_rs_encode_packed",
     "qrm_verify_threshold", "qrm_make_corpus_device", "qrm_patterns_device", "qrm_allocate_streams",
@@ -98,6 +98,8 @@ def lib() -> C.CDLL:
         L.qrm_ctx_destroy.argtypes = [vp]
         L.qrm_ctx_info.argtypes = [vp, C.POINTER(u64), C.POINTER(u64), C.POINTER(i32), C.POINTER(i32)]
         L.qrm_ctx_set_extractor.argtypes = [vp, i32, u64]
+        L.qrm_attack_device.argtypes = [vp, i64, i32, i32, i64, i32, C.c_double, vp, i64, C.POINTER(i32),
+                                        C.POINTER(i32), vp]
         L.qrm_ppm_read.argtypes = [C.c_char_p, vp, i64, C.POINTER(i32), C.POINTER(i32)]
         L.qrm_ppm_write.argtypes = [C.c_char_p, vp, i32, i32]
         L.qrm_ppm_read_batch.argtypes = [C.POINTER(C.c_char_p), i64, i32, i32, vp, i64, i32, vp]
@@ -532,6 +534,30 @@ def semantic_fields(rec: np.ndarray, code: CodeParams) -> dict:
             "msg": np.where(rec["status"] == 1, rec["msg"], 0).astype(np.uint64),
             "errors": rec["errors"].astype(np.int32), "bit_acc": rec["matches"] / float(nb),
             "verified": rec["verified"].astype(bool)}
+
+
+ATTACKS = ("centercrop", "resizeto", "normalize", "crop", "resize", "brightness", "contrast", "saturation",
+           "sharpness", "blur", "overlay_text", "jpeg_approx")  # TransformOp order (transforms.hpp:22-35)
+ATTACK_SUITE = (("C-0.1", "crop", 0.1), ("C-0.5", "crop", 0.5), ("R-0.5", "resize", 0.5), ("BL", "blur", 1.0),
+                ("BR-2", "brightness", 2.0), ("CON-2", "contrast", 2.0))  # attack_suite (transforms.cpp:364-373)
+
+
+def apply_attack(images, op: str, param: float, stream=None):
+    """apply_attack (transforms.cpp:289-362) on a uint8 CUDA tensor [B, H, W, 3] -> CUDA tensor
+    (uint8, or float32 for "normalize"), bit-exact with the reference."""
+    import torch
+    if op not in ATTACKS:
+        raise InvalidInput(f"unknown transform op: {op}")
+    B, H, W, _ = images.shape
+    code = ATTACKS.index(op)
+    ow, oh = C.c_int(), C.c_int()
+    _check(lib().qrm_attack_device(_ptr(images), B, W, H, images.stride(0), code, param, None, 0, C.byref(ow),
+                                   C.byref(oh), _stream(stream)))
+    dt = torch.float32 if op == "normalize" else torch.uint8
+    out = torch.empty((B, oh.value, ow.value, 3), dtype=dt, device=images.device)
+    _check(lib().qrm_attack_device(_ptr(images), B, W, H, images.stride(0), code, param, _ptr(out),
+                                   out.stride(0) * out.element_size(), C.byref(ow), C.byref(oh), _stream(stream)))
+    return out
 
 
 # --------------------------------------------------------------- formats --

@@ -40,6 +40,9 @@ cudaError_t launch_detect_finish(const DetectParams& p, int tmax, int sm_count, 
 cudaError_t launch_gather_windows(const GatherDesc* descs, int64_t count, int l, uint8_t* out, cudaStream_t st);
 cudaError_t launch_fetch_windows(const WindowSource& src, int64_t count, int K, uint8_t* out, int sm_count,
                                  cudaStream_t st);
+cudaError_t launch_attack_pixels(const AttackParams& p, cudaStream_t st);
+cudaError_t launch_attack_jpeg(const AttackParams& p, cudaStream_t st);
+cudaError_t launch_attack_resample(const AttackParams& p, cudaStream_t st);
 cudaError_t launch_rs_packed(const RsTables* tab, int m, int r, int t, int algo, const uint64_t* words,
                              int64_t count, uint64_t* cw, int8_t* nerr, int sm_count, cudaStream_t st);
 cudaError_t launch_rs_symbols(const RsTables* tab, int n, int t, const uint8_t* recv, int64_t count, uint8_t* cw,
@@ -1175,6 +1178,171 @@ QRM_EXPORT qrm_status qrm_resample_host(const uint8_t* image, int w, int h, int 
     QRM_CUDA(cudaMemcpy(out, dout, ob, cudaMemcpyDeviceToHost));
     cudaFree(dimg);
     cudaFree(dout);
+    return QRM_OK;
+}
+
+QRM_EXPORT qrm_status qrm_attack_device(const uint8_t* images, int64_t count, int w, int h, int64_t stride, int op,
+                                        double param, void* out, int64_t out_stride, int* out_w, int* out_h,
+                                        void* stream) {
+    // Argument checks, output geometry and host-side constants follow
+    // apply_attack (transforms.cpp:289-362) and its helpers.
+    if (count < 0 || w <= 0 || h <= 0 || !out_w || !out_h) return fail(QRM_INVALID_INPUT, "bad attack arguments");
+    AttackParams p{};
+    p.in = images;
+    p.in_stride = stride;
+    p.w = w;
+    p.h = h;
+    p.count = count;
+    p.op = op;
+    p.param = param;
+    p.sw = w;
+    p.sh = h;
+    int ow = w, oh = h;
+    int stages = 1;  // resize: two resample passes
+    int dw = 0, dh = 0;
+    auto crop_to = [&](int cw, int ch) -> qrm_status {
+        if (cw > w || ch > h) return fail(QRM_INVALID_INPUT, "crop window larger than image");
+        ow = cw;
+        oh = ch;
+        p.x_off = (w - cw) / 2;
+        p.y_off = (h - ch) / 2;
+        return QRM_OK;
+    };
+    qrm_status s = QRM_OK;
+    switch (op) {
+        case QRM_ATTACK_CENTERCROP: {
+            const int side = static_cast<int>(param);
+            if (side <= 0) return fail(QRM_INVALID_INPUT, "centercrop size must be positive");
+            s = crop_to(std::min(side, w), std::min(side, h));
+            break;
+        }
+        case QRM_ATTACK_RESIZETO: {
+            const int side = static_cast<int>(param);
+            if (side <= 0) return fail(QRM_INVALID_INPUT, "resizeto size must be positive");
+            ow = oh = side;
+            p.resize = 1;
+            p.sw = p.sh = side;
+            break;
+        }
+        case QRM_ATTACK_NORMALIZE: p.normalize = 1; break;
+        case QRM_ATTACK_CROP: {
+            if (param <= 0.0 || param > 1.0) return fail(QRM_INVALID_INPUT, "crop fraction must be in (0, 1]");
+            const double f = std::sqrt(param);
+            s = crop_to(std::max(1, static_cast<int>(std::lround(w * f))), std::max(1, static_cast<int>(std::lround(h * f))));
+            break;
+        }
+        case QRM_ATTACK_RESIZE:
+            if (param <= 0.0 || param >= 1.0) {
+                if (param != 1.0) return fail(QRM_INVALID_INPUT, "resize factor must be in (0, 1)");
+                break;  // identity
+            }
+            dw = std::max(1, static_cast<int>(std::lround(w * param)));
+            dh = std::max(1, static_cast<int>(std::lround(h * param)));
+            stages = 2;
+            break;
+        case QRM_ATTACK_BRIGHTNESS:
+            if (param < 0.0) return fail(QRM_INVALID_INPUT, "brightness factor must be nonnegative");
+            break;
+        case QRM_ATTACK_CONTRAST:
+            if (param < 0.0) return fail(QRM_INVALID_INPUT, "contrast factor must be nonnegative");
+            break;
+        case QRM_ATTACK_SATURATION:
+            if (param < 0.0) return fail(QRM_INVALID_INPUT, "saturation factor must be nonnegative");
+            break;
+        case QRM_ATTACK_SHARPNESS:
+            if (param < 0.0) return fail(QRM_INVALID_INPUT, "sharpness factor must be nonnegative");
+            break;
+        case QRM_ATTACK_BLUR:
+        case QRM_ATTACK_OVERLAY_TEXT: break;
+        case QRM_ATTACK_JPEG_APPROX:
+            if (param <= 0.0 || param > 100.0) return fail(QRM_INVALID_INPUT, "jpeg_approx quality must be in (0, 100]");
+            break;
+        default: return fail(QRM_INVALID_INPUT, "unknown transform op");
+    }
+    if (s != QRM_OK) return s;
+    *out_w = ow;
+    *out_h = oh;
+    if (!out || count == 0) return QRM_OK;
+    if (!images) return fail(QRM_INVALID_INPUT, "null image pointer");
+    if (stride < static_cast<int64_t>(w) * h * 3) return fail(QRM_INVALID_INPUT, "image stride smaller than an image");
+    const int64_t out_bytes = static_cast<int64_t>(ow) * oh * 3 * (op == QRM_ATTACK_NORMALIZE ? 4 : 1);
+    if (out_stride < out_bytes) return fail(QRM_INVALID_INPUT, "output stride smaller than an output image");
+    cudaStream_t st = as_stream(stream);
+    p.out = static_cast<uint8_t*>(out);
+    p.out_stride = out_stride;
+    p.ow = ow;
+    p.oh = oh;
+    // host libm constants, exactly as the reference evaluates them
+    p.kC = 1.0;
+    p.kE = std::exp(-0.5);
+    p.kD = std::exp(-1.0);
+    p.kSum = p.kC + 4.0 * p.kE + 4.0 * p.kD;
+    double* dtmp = nullptr;  // pivots / jpeg tables
+    uint8_t* mid = nullptr;  // resize: the downscaled intermediate
+    struct Free {
+        double*& a;
+        uint8_t*& b;
+        ~Free() {
+            cudaFree(a);
+            cudaFree(b);
+        }
+    } release{dtmp, mid};
+    switch (op) {
+        case QRM_ATTACK_CENTERCROP: case QRM_ATTACK_RESIZETO: case QRM_ATTACK_NORMALIZE: case QRM_ATTACK_CROP:
+            QRM_LAUNCH(launch_attack_resample(p, st));
+            break;
+        case QRM_ATTACK_RESIZE:
+            if (stages == 1) {
+                QRM_LAUNCH(launch_attack_resample(p, st));  // factor 1: a copy
+            } else {
+                // resize_bilinear(resize_bilinear(img, dw, dh), w, h)
+                QRM_CUDA(cudaMalloc(&mid, static_cast<size_t>(dw) * dh * 3 * count));
+                AttackParams a = p;
+                a.out = mid;
+                a.out_stride = static_cast<int64_t>(dw) * dh * 3;
+                a.ow = a.sw = dw;
+                a.oh = a.sh = dh;
+                a.resize = 1;
+                QRM_LAUNCH(launch_attack_resample(a, st));
+                AttackParams b = p;
+                b.in = mid;
+                b.in_stride = a.out_stride;
+                b.w = dw;
+                b.h = dh;
+                b.resize = 1;
+                b.sw = w;
+                b.sh = h;
+                QRM_LAUNCH(launch_attack_resample(b, st));
+            }
+            break;
+        case QRM_ATTACK_JPEG_APPROX: {
+            static const int kQ[64] = {16, 11, 10, 16, 24,  40,  51,  61,  12, 12, 14, 19, 26,  58,  60,  55,
+                                       14, 13, 16, 24, 40,  57,  69,  56,  14, 17, 22, 29, 51,  87,  80,  62,
+                                       18, 22, 37, 56, 68,  109, 103, 77,  24, 35, 55, 64, 81,  104, 113, 92,
+                                       49, 64, 78, 87, 103, 121, 120, 101, 72, 92, 95, 98, 112, 100, 103, 99};
+            const double scale = param < 50.0 ? 5000.0 / param : 200.0 - 2.0 * param;
+            std::vector<double> tab(128);
+            for (int i = 0; i < 64; ++i) tab[64 + i] = std::clamp(std::floor((kQ[i] * scale + 50.0) / 100.0), 1.0, 255.0);
+            constexpr double kPi = 3.14159265358979323846;
+            for (int u = 0; u < 8; ++u)
+                for (int i = 0; i < 8; ++i) tab[u * 8 + i] = std::cos((2 * i + 1) * u * kPi / 16.0);
+            QRM_CUDA(cudaMalloc(&dtmp, sizeof(double) * 128));
+            QRM_CUDA(cudaMemcpyAsync(dtmp, tab.data(), sizeof(double) * 128, cudaMemcpyHostToDevice, st));
+            p.jpeg_cos = dtmp;
+            p.jpeg_quant = dtmp + 64;
+            p.dct_c0 = std::sqrt(0.125);
+            QRM_LAUNCH(launch_attack_jpeg(p, st));
+            QRM_CUDA(cudaStreamSynchronize(st));  // the pageable table copy and dtmp outlive no call
+            break;
+        }
+        default:
+            if (op == QRM_ATTACK_CONTRAST) {
+                QRM_CUDA(cudaMalloc(&dtmp, sizeof(double) * count));
+                p.pivot = dtmp;
+            }
+            QRM_LAUNCH(launch_attack_pixels(p, st));
+    }
+    if (dtmp || mid) QRM_CUDA(cudaStreamSynchronize(st));  // temporaries are freed on return
     return QRM_OK;
 }
 

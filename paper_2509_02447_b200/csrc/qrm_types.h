@@ -79,4 +79,25 @@ struct DetectParams {
     PendingEntry* pending;    // capacity = count
 };
 
+
+// apply_attack (transforms.cpp:289-362) over a batch of same-size byte images.
+struct AttackParams {
+    const uint8_t* in;
+    int64_t in_stride;
+    int32_t w, h;
+    uint8_t* out;  // u8 (or float for normalize)
+    int64_t out_stride;
+    int32_t ow, oh;
+    int64_t count;
+    int32_t op;
+    double param;
+    // geometry: output (x, y) = pixel (x + x_off, y + y_off) of the image resized to sw x sh
+    int32_t resize, sw, sh, x_off, y_off, normalize;
+    double* pivot;  // [count] mean luma (contrast)
+    double kC, kE, kD, kSum;  // gaussian3x3 weights (host exp)
+    const double* jpeg_cos;   // [8][8] host cos((2i+1) u pi / 16)
+    const double* jpeg_quant; // [64]
+    double dct_c0;            // sqrt(0.125)
+};
+
 }  // namespace qrm
