@@ -206,6 +206,46 @@ def hidden_submetric(ctx, pool, world, max_over_ranks, stream, batch=BATCH, reps
                          "frac": tflops / peak, "peak_kind": kind}}
 
 
+def config512_submetric(q, ctx, cfg, world, rank, max_over_ranks, warmup, batch=16384, pool_n=2048):
+    """configs[2]: 512x512 images, batch 16384, host images -> host records through
+    the stream executor with the plan Algorithm 1 (allocate_streams, sched.cpp:50)
+    derives from a cudaEvent warm-up profile (warmup_profile, sim.cpp:240), next to
+    the reference's single-stream baseline plan (cmd_bench, cli.cpp:440-446)."""
+    import numpy as np
+    import torch
+    dev_pool = q.make_corpus(cfg, 100000 + rank * pool_n, pool_n, 512, 512)
+    host = torch.empty(dev_pool.shape, dtype=torch.uint8, pin_memory=True)
+    host.copy_(dev_pool)
+    del dev_pool
+    torch.cuda.empty_cache()
+    t, m = ctx.warmup_profile(iters=5, b0=16, mode=0, ptr=host.data_ptr(), shape=(pool_n, 512, 512))
+    free = float(torch.cuda.mem_get_info()[0])
+    plan = q.allocate_streams(t, m, 16.0, batch, 16, free, 0.0, 2)
+    recs_pin = torch.empty((pool_n, q.RECORD_DTYPE.itemsize), dtype=torch.uint8, pin_memory=True)
+    recs = recs_pin.numpy().view(q.RECORD_DTYPE).reshape(-1)
+    calls = batch // pool_n
+
+    def run(pl, steps):
+        for i in range(steps * calls):
+            ctx.detect_host(None, (i * world + rank) * pool_n, plan=pl, mode=0, out=recs, ptr=host.data_ptr(),
+                            shape=(pool_n, 512, 512))
+            assert recs["verified"].all()
+
+    out = {"workload": "configs[2]: 512x512 RGB, batch 16384 (8 calls x 2048 over a pinned pool), one 64x64 tile "
+                       "per image after the centre crop, mode 0 transfer",
+           "warmup_profile_ms_per_16": [float(x) for x in t], "warmup_bytes_per_image": [float(x) for x in m]}
+    for name, pl in (("alg1", (plan.streams, [max(1, min(pool_n, x)) for x in plan.minibatch])),
+                     ("baseline_111", ([1, 1, 1], [pool_n] * 3))):
+        run(pl, max(1, warmup // 3))
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        run(pl, 2)
+        dt = max_over_ranks(time.perf_counter() - t0)
+        out[name] = {"plan": {"streams": list(pl[0]), "minibatch": list(pl[1])},
+                     "e2e_images_per_s": world * 2 * batch / dt}
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -367,6 +407,34 @@ def main():
     except Exception as exc:
         hidden = {"unavailable": str(exc)}
 
+    try:
+        config512 = config512_submetric(q, ctx, cfg, world, rank, max_over_ranks, args.warmup)
+    except Exception as exc:
+        config512 = {"unavailable": str(exc)}
+
+    # Robustness sweep (the paper's Table 3 analogue): each
+    # attack of attack_suite on the device, then detection; TPR and bit accuracy.
+    robustness = {}
+    try:
+        imgs = pool[:BATCH]
+        out_r = torch.empty((BATCH, q.RECORD_DTYPE.itemsize), dtype=torch.uint8, device=dev)
+        for name, op, prm in q.ATTACK_SUITE:
+            att = q.apply_attack(imgs, op, prm)
+            ctx.detect_device(att, first_draw=0, out=out_r)
+            torch.cuda.synchronize()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            att = q.apply_attack(imgs, op, prm)
+            ctx.detect_device(att, first_draw=0, out=out_r)
+            b.record(stream)
+            torch.cuda.synchronize()
+            r = q.records_from_device(out_r)
+            robustness[name] = {"tpr": float(r["verified"].mean()),
+                                "bit_acc": float(r["matches"].mean() / cfg.code.codeword_bits()),
+                                "attack_plus_detect_ms": a.elapsed_time(b), "images": BATCH}
+    except Exception as exc:
+        robustness = {"unavailable": str(exc)}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
@@ -403,6 +471,8 @@ def main():
                          "algorithmic_bytes_per_launch": alg_bytes},
             "rs": {"words": args.rs_words, "profile": "gf16-15-12", **rs},
             "learned_extractor": hidden,
+            "robustness": robustness,
+            "config_512": config512,
             "cpu_baseline": cpu,
             "clocks": clocks.summary(),
         }

@@ -287,6 +287,11 @@ QRM_EXPORT qrm_status qrm_lpt_schedule(int ntasks, const int* ids, const double*
 QRM_EXPORT qrm_status qrm_warmup_profile(qrm_ctx* ctx, const uint8_t* images, int64_t count, int w, int h,
                                          int64_t image_stride, int warmup_iters, int b0, double* time,
                                          double* memory);
+/* As qrm_warmup_profile with the transfer stage of host-pipeline mode `mode`
+ * (0: zero-copy window fetch, memory[0] = 3 l^2 B/image; 1: full-image copy). */
+QRM_EXPORT qrm_status qrm_warmup_profile_mode(qrm_ctx* ctx, const uint8_t* images, int64_t count, int w, int h,
+                                              int64_t image_stride, int iters, int b0, int mode, double* time,
+                                              double* memory);
 /* Sets the plan used by qrm_detect_host when its plan argument is NULL. */
 QRM_EXPORT qrm_status qrm_ctx_set_plan(qrm_ctx* ctx, const qrm_plan* plan);
 

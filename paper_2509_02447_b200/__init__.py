@@ -27,7 +27,7 @@ LIB_PATH = os.path.join(_HERE, "_lib", "libqrmark_b200.so")
 # Exported symbols of include/qrmark_gpu.h (checked by the CPU test suite).
 ABI_SYMBOLS = (
     "qrm_last_error", "qrm_abi_version", "qrm_device_count", "qrm_ctx_create", "qrm_ctx_destroy", "qrm_ctx_info",
-    "qrm_ctx_set_extractor", "qrm_ppm_read", "qrm_ppm_write", "qrm_ppm_read_batch", "qrm_records_json", "qrm_cache_hits", "qrm_attack_device",
+    "qrm_ctx_set_extractor", "qrm_ppm_read", "qrm_ppm_write", "qrm_ppm_read_batch", "qrm_records_json", "qrm_cache_hits", "qrm_attack_device", "qrm_warmup_profile_mode",
     "qrm_detect_device", "qrm_detect_host", "qrm_detect_ragged", "qrm_extract_device", "qrm_preprocess_host",
     "qrm_rs_decode_packed_device", "qrm_rs_decode_symbols_device", "qrm_rs_stress_device", "qrm_rs_encode_packed",
     "qrm_verify_threshold", "qrm_make_corpus_device", "qrm_patterns_device", "qrm_allocate_streams",
@@ -122,6 +122,7 @@ def lib() -> C.CDLL:
         L.qrm_lpt_schedule.argtypes = [i32, vp, vp, vp, vp, i32, C.c_double, C.c_double, i32, i32, i32, vp, vp, vp,
                                        vp, vp, vp, C.POINTER(i32), vp, C.POINTER(i32)]
         L.qrm_warmup_profile.argtypes = [vp, vp, i64, i32, i32, i64, i32, i32, vp, vp]
+        L.qrm_warmup_profile_mode.argtypes = [vp, vp, i64, i32, i32, i64, i32, i32, i32, vp, vp]
         L.qrm_ctx_set_plan.argtypes = [vp, C.POINTER(_Plan)]
         L.qrm_probe_decode_kernel.argtypes = [vp, vp, i64, i32, i32, i64, i32, C.POINTER(C.c_double)]
         L.qrm_hidden_detect_device.argtypes = [vp, vp, i64, i32, i32, i64, u64, u64, vp, vp, vp]
@@ -501,14 +502,21 @@ class DetectionContext:
         pl = _Plan((C.c_int * 3)(*streams), (C.c_int * 3)(*minibatch))
         _check(lib().qrm_ctx_set_plan(self._h, C.byref(pl)))
 
-    def warmup_profile(self, images: np.ndarray, iters: int = 3, b0: int = 16):
-        """warmup_profile (sim.cpp:240-288) on the device stages -> (time[3] ms per b0, memory[3] B/image)."""
-        images = np.ascontiguousarray(images, dtype=np.uint8)
-        B, H, W, _ = images.shape
+    def warmup_profile(self, images: np.ndarray | None = None, iters: int = 3, b0: int = 16, mode: int = 1,
+                       ptr: int | None = None, shape=None):
+        """warmup_profile (sim.cpp:240-288) on the device stages -> (time[3] ms per b0, memory[3] B/image).
+        mode: the host pipeline's transfer (0 window fetch, 1 full-image copy)."""
+        if images is not None:
+            images = np.ascontiguousarray(images, dtype=np.uint8)
+            B, H, W, _ = images.shape
+            p = images.ctypes.data
+        else:
+            B, H, W = shape
+            p = ptr
         t = np.zeros(3)
         m = np.zeros(3)
-        _check(lib().qrm_warmup_profile(self._h, images.ctypes.data, B, W, H, H * W * 3, iters, b0, t.ctypes.data,
-                                        m.ctypes.data))
+        _check(lib().qrm_warmup_profile_mode(self._h, p, B, W, H, H * W * 3, iters, b0, mode, t.ctypes.data,
+                                             m.ctypes.data))
         return t, m
 
 

@@ -1402,20 +1402,44 @@ QRM_EXPORT qrm_status qrm_lpt_schedule(int ntasks, const int* ids, const double*
     return QRM_OK;
 }
 
-QRM_EXPORT qrm_status qrm_warmup_profile(qrm_ctx* c, const uint8_t* images, int64_t count, int w, int h,
-                                         int64_t stride, int iters, int b0, double* time, double* memory) {
+QRM_EXPORT qrm_status qrm_warmup_profile_mode(qrm_ctx* c, const uint8_t* images, int64_t count, int w, int h,
+                                              int64_t stride, int iters, int b0, int mode, double* time,
+                                              double* memory) {
     // warmup_profile (sim.cpp:240-288) for the device stages: medians of
-    // cudaEvent-timed runs of transfer / decode / correct+return at batch b0.
+    // cudaEvent-timed runs of transfer / decode / correct+return at batch b0,
+    // with the transfer of host-pipeline mode `mode` (0: zero-copy window
+    // fetch, 1: full-image copy).
     qrm_status s = check_uniform(c, images, count, w, h, stride);
     if (s != QRM_OK) return s;
     if (iters < 1) return fail(QRM_INVALID_INPUT, "need at least one warm-up iteration");
     if (count == 0) return fail(QRM_INVALID_INPUT, "warm-up needs at least one image");
+    if (mode != 0 && mode != 1) return fail(QRM_INVALID_INPUT, "warm-up mode must be 0 (window fetch) or 1 (full image)");
     if ((s = set_device(c->device)) != QRM_OK) return s;
     b0 = static_cast<int>(std::min<int64_t>(std::max(1, b0), count));
     const int64_t img_bytes = static_cast<int64_t>(w) * h * 3;
     Workspace& W = c->ws[0];
     if ((s = ensure(W.images, W.images_cap, b0 * img_bytes)) != QRM_OK) return s;
+    if ((s = ensure(W.stage, W.stage_cap, static_cast<int64_t>(b0) * c->K)) != QRM_OK) return s;
     if ((s = ensure(c->d_records, c->records_cap, b0)) != QRM_OK) return s;
+    int up, sw, sh, xo, yo;
+    geometry(w, h, up, sw, sh, xo, yo);
+    const uint8_t* mapped = nullptr;
+    bool reg = false;
+    if (mode == 0) {
+        cudaPointerAttributes attr{};
+        if (cudaPointerGetAttributes(&attr, images) != cudaSuccess || attr.type != cudaMemoryTypeHost) {
+            cudaGetLastError();
+            QRM_CUDA(cudaHostRegister(const_cast<uint8_t*>(images), (b0 - 1) * stride + img_bytes,
+                                      cudaHostRegisterMapped | cudaHostRegisterReadOnly));
+            reg = true;
+        }
+        QRM_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(const_cast<uint8_t**>(&mapped)),
+                                          const_cast<uint8_t*>(images), 0));
+        if (!direct_ok(c, mapped, w, h, stride) || (3 * c->l) % 16 != 0) {
+            if (reg) cudaHostUnregister(const_cast<uint8_t*>(images));
+            return fail(QRM_INVALID_INPUT, "window fetch needs 16-B aligned windows (use mode 1)");
+        }
+    }
     std::vector<qrm_record> host(b0);
     cudaStream_t st = nullptr;
     cudaEvent_t a, b;
@@ -1430,20 +1454,41 @@ QRM_EXPORT qrm_status qrm_warmup_profile(qrm_ctx* c, const uint8_t* images, int6
         cudaEventElapsedTime(&ms, a, b);
         return ms;
     };
+    WindowSource hs{};
+    hs.base = mapped;
+    hs.image_stride = stride;
+    hs.pitch = w * 3;
+    hs.x_off = xo;
+    hs.y_off = yo;
+    hs.direct = 1;
+    hs.l = c->l;
+    hs.strategy = c->cfg.tile_strategy;
+    hs.tile_seed = c->cfg.tile_seed;
+    WindowSource staged = hs;
+    staged.base = W.stage;
+    staged.image_stride = c->K;
+    staged.pitch = 3 * c->l;
+    staged.direct = 0;
     std::vector<double> t0v, t1v, t2v;
     for (int i = 0; i < iters; ++i) {
-        t0v.push_back(timed([&] {
-            cudaMemcpy2DAsync(W.images, img_bytes, images, stride, img_bytes, b0, cudaMemcpyHostToDevice, st);
-        }));
-        t1v.push_back(timed([&] {
-            detect_uniform(c, W, W.images, b0, w, h, img_bytes, 0, c->d_records, nullptr, nullptr, st);
-        }));
+        if (mode == 0) {
+            t0v.push_back(timed([&] { launch_fetch_windows(hs, b0, c->K, W.stage, c->sms, st); }));
+            t1v.push_back(timed([&] { run_detect(c, W, staged, b0, c->d_records, nullptr, nullptr, st); }));
+        } else {
+            t0v.push_back(timed([&] {
+                cudaMemcpy2DAsync(W.images, img_bytes, images, stride, img_bytes, b0, cudaMemcpyHostToDevice, st);
+            }));
+            t1v.push_back(timed([&] {
+                detect_uniform(c, W, W.images, b0, w, h, img_bytes, 0, c->d_records, nullptr, nullptr, st);
+            }));
+        }
         t2v.push_back(timed([&] {
             cudaMemcpyAsync(host.data(), c->d_records, sizeof(qrm_record) * b0, cudaMemcpyDeviceToHost, st);
         }));
     }
     cudaEventDestroy(a);
     cudaEventDestroy(b);
+    if (reg) cudaHostUnregister(const_cast<uint8_t*>(images));
     auto med = [](std::vector<double> v) {
         std::sort(v.begin(), v.end());
         double x = v[v.size() / 2];
@@ -1453,11 +1498,16 @@ QRM_EXPORT qrm_status qrm_warmup_profile(qrm_ctx* c, const uint8_t* images, int6
     time[0] = med(t0v);
     time[1] = med(t1v);
     time[2] = med(t2v);
-    memory[0] = static_cast<double>(img_bytes);
+    memory[0] = static_cast<double>(mode == 0 ? c->K : img_bytes);
     memory[1] = static_cast<double>(c->K + sizeof(PendingEntry));
     memory[2] = static_cast<double>(sizeof(qrm_record));
     QRM_CUDA(cudaGetLastError());
     return QRM_OK;
+}
+
+QRM_EXPORT qrm_status qrm_warmup_profile(qrm_ctx* c, const uint8_t* images, int64_t count, int w, int h,
+                                         int64_t stride, int iters, int b0, double* time, double* memory) {
+    return qrm_warmup_profile_mode(c, images, count, w, h, stride, iters, b0, 1, time, memory);
 }
 
 }  // extern "C"

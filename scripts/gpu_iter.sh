@@ -1,2 +1,7 @@
 cd $GRAFT_REPO_ROOT
-timeout 900 python -m pytest tests/test_attacks.py -x -q -m gpu 2>&1 | tail -15
+( time timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err ) 2> gpurun_out/bench_time.txt
+tail -3 gpurun_out/bench.err; cat gpurun_out/bench_time.txt
+python -c "
+import json; d = json.load(open('gpurun_out/bench.json'))
+for k in ('value','e2e','roofline','config_512','robustness','learned_extractor','cpu_baseline','gpu_launches'): print(k, json.dumps(d.get(k))[:600])
+"
