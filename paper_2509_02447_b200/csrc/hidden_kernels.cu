@@ -72,17 +72,20 @@ __device__ __forceinline__ void quarter_sync(int q) {
     asm volatile("bar.sync %0, 64;" ::"r"(1 + q) : "memory");
 }
 
+// kSlabs staging buffers of 16 KB rotate per block, so a quarter's TMA store
+// may still be reading slab i while block i+1 writes slab i+1.
+template <int kSlabs>
 __device__ __forceinline__ void conv_epilogue(const HiddenLayerParams& p, const CUtensorMap* tmap_out,
                                               const uint32_t (&acc)[kHCh], const float* s_bias, float (*pool)[kHC],
-                                              uint32_t o_s, int q, int h, int lane, int64_t tile, int blk) {
+                                              uint32_t o_s, int q, int h, int lane, int64_t tile, int blk, int iter) {
     const int pix = blk * kHM + q * 32 + lane;
     float v[kHCh];
 #pragma unroll
     for (int c = 0; c < kHCh; ++c) v[c] = fmaxf(__uint_as_float(acc[c]) + s_bias[h * kHCh + c], 0.0f);
     if (!p.last) {
         // 16-B chunk c of row r at chunk c ^ (r & 7): conflict-free STS.128
-        const uint32_t slab = o_s + q * 4096;
-        if (h == 0 && lane == 0) bulk_wait_read<0>();  // the quarter's previous store has read the slab
+        const uint32_t slab = o_s + (iter % kSlabs) * kHOBytes + q * 4096;
+        if (h == 0 && lane == 0) bulk_wait_read<kSlabs - 1>();  // the store that used this slab has read it
         quarter_sync(q);
         const uint32_t row = slab + lane * 128;
 #pragma unroll
@@ -241,8 +244,8 @@ __global__ void __launch_bounds__(kHThreads, 1)
             __syncwarp();
             if (lane == 0) mbar_arrive(&sm.acc_empty[a]);
             if (!(p.dbg & 16))  // timing experiment: skip the epilogue math/stores
-                conv_epilogue(p, &tmap_out, acc, s_bias, sm.pool, o_s, q, h, lane, b / kHBlocks,
-                              static_cast<int>(b % kHBlocks));
+                conv_epilogue<1>(p, &tmap_out, acc, s_bias, sm.pool, o_s, q, h, lane, b / kHBlocks,
+                                 static_cast<int>(b % kHBlocks), i);
         }
         if (!p.last && h == 0 && lane == 0) bulk_wait<0>();
     }
@@ -267,7 +270,8 @@ __global__ void __launch_bounds__(kHThreads, 1)
 //   acc_full[a] (each CTA)  multicast commit
 //   acc_empty[a](even CTA)  16 arrivals: the 8 epilogue warps of both CTAs
 constexpr int kPWBytes = kHWBytes / 2;  // 36 KB: 9 taps x 32 co x 64 ci
-constexpr int kPAStages = 5;
+constexpr int kPAStages = 4;
+constexpr int kPSlabs = 2;  // output staging slabs (16 KB each)
 struct PairSmem {
     uint64_t w_full;
     uint64_t a_full[kPAStages], a_empty[kPAStages];
@@ -275,7 +279,7 @@ struct PairSmem {
     uint32_t tmem_base;
     float pool[4][kHC];
 };
-constexpr size_t kPSmemBytes = 1024 + kPWBytes + kPAStages * kHABytes + kHOBytes + 128 + sizeof(PairSmem);
+constexpr size_t kPSmemBytes = 1024 + kPWBytes + kPAStages * kHABytes + kPSlabs * kHOBytes + 128 + sizeof(PairSmem);
 static_assert(kPSmemBytes <= 232448, "conv64 pair shared memory exceeds 227 KB");
 constexpr int kPairBlocks = kHBlocks / 2;  // 16 pair-blocks (4 rows) per tile
 
@@ -288,7 +292,7 @@ __global__ void __launch_bounds__(kHThreads, 1)
     const uint32_t w_s = smem_u32(base);
     const uint32_t a_s0 = w_s + kPWBytes;
     const uint32_t o_s = a_s0 + kPAStages * kHABytes;
-    PairSmem& sm = *reinterpret_cast<PairSmem*>(base + kPWBytes + kPAStages * kHABytes + kHOBytes + 128);
+    PairSmem& sm = *reinterpret_cast<PairSmem*>(base + kPWBytes + kPAStages * kHABytes + kPSlabs * kHOBytes + 128);
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const uint32_t rank = cluster_ctarank();  // 0 = even CTA (MMA issuer), 1 = odd
@@ -388,8 +392,8 @@ __global__ void __launch_bounds__(kHThreads, 1)
             __syncwarp();
             if (lane == 0) mbar_arrive_cluster(empty0[a]);
             if (!(p.dbg & 16))
-            conv_epilogue(p, &tmap_out, acc, s_bias, sm.pool, o_s, q, h, lane, b / kPairBlocks,
-                          static_cast<int>(b % kPairBlocks) * 2 + static_cast<int>(rank));
+            conv_epilogue<kPSlabs>(p, &tmap_out, acc, s_bias, sm.pool, o_s, q, h, lane, b / kPairBlocks,
+                                   static_cast<int>(b % kPairBlocks) * 2 + static_cast<int>(rank), i);
         }
         if (!p.last && h == 0 && lane == 0) bulk_wait<0>();
     }

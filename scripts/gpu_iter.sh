@@ -1,7 +1,3 @@
 cd $GRAFT_REPO_ROOT
-( time timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err ) 2> gpurun_out/bench_time.txt
-tail -3 gpurun_out/bench.err; cat gpurun_out/bench_time.txt
-python -c "
-import json; d = json.load(open('gpurun_out/bench.json'))
-for k in ('value','e2e','roofline','config_512','robustness','learned_extractor','cpu_baseline','gpu_launches'): print(k, json.dumps(d.get(k))[:600])
-"
+for pr in 1 0; do echo "pair=$pr"; QRM_CONV_PAIR=$pr ncu --metrics gpu__time_duration.sum,sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed --clock-control none -k regex:conv64 -s 3 -c 1 python scripts/bench_hidden.py 1024 2>/dev/null | grep -E "duration|tensor"; done
+QRM_CONV_PAIR=1 timeout 300 python -m pytest tests/test_hidden.py -x -q -m gpu 2>&1 | tail -1
