@@ -278,7 +278,27 @@ qrm_status run_detect(qrm_ctx* c, Workspace& w, const WindowSource& src, int64_t
         QRM_CUDA(cudaMemsetAsync(d_dbg, 0, sizeof(unsigned long long) * 8 * max_ctas, st));
         p.dbg_times = d_dbg;
     }
+    long long* d_stg = nullptr;
+    if (getenv("QRM_DEBUG_STAGES")) {  // diagnostics: per-stage issue / arrival clocks of CTAs 0-7
+        QRM_CUDA(cudaMalloc(&d_stg, sizeof(long long) * 8 * 256));
+        QRM_CUDA(cudaMemsetAsync(d_stg, 0, sizeof(long long) * 8 * 256, st));
+        p.dbg_stages = d_stg;
+    }
     QRM_LAUNCH(launch_corr_detect(p, c->sms, st));
+    if (d_stg) {
+        std::vector<long long> h(8 * 256);
+        QRM_CUDA(cudaMemcpyAsync(h.data(), d_stg, sizeof(long long) * h.size(), cudaMemcpyDeviceToHost, st));
+        QRM_CUDA(cudaStreamSynchronize(st));
+        cudaFree(d_stg);
+        for (int b = 0; b < 2; ++b) {
+            const long long t0 = h[b * 256];
+            fprintf(stderr, "[qrm stages] count=%lld cta %d issue:", static_cast<long long>(count), b);
+            for (int i = 0; i < 128 && h[b * 256 + i]; ++i) fprintf(stderr, " %lld", h[b * 256 + i] - t0);
+            fprintf(stderr, "\n[qrm stages] count=%lld cta %d full: ", static_cast<long long>(count), b);
+            for (int i = 0; i < 128 && h[b * 256 + 128 + i]; ++i) fprintf(stderr, " %lld", h[b * 256 + 128 + i] - t0);
+            fprintf(stderr, "\n");
+        }
+    }
     if (d_dbg) {
         dbg.resize(8 * max_ctas);
         QRM_CUDA(cudaMemcpyAsync(dbg.data(), d_dbg, sizeof(unsigned long long) * dbg.size(), cudaMemcpyDeviceToHost, st));

@@ -176,6 +176,7 @@ __global__ void __launch_bounds__(kCorrThreads, 1) corr_detect_kernel(const __gr
         for (int it = 0; it < kchunks; ++it) {
             const int s = it % kCorrStages;
             mbar_wait(&sm.empty[s], ((it / kCorrStages) & 1) ^ 1);
+            if (p.dbg_stages && tid == 0 && blockIdx.x < 8 && it < 128) p.dbg_stages[blockIdx.x * 256 + it] = clock64();
             const uint32_t a_s = ring_u32 + s * kCorrStageBytes;
             const uint32_t b_s = a_s + kCorrABytes;
             if (kbyte < p.K) {
@@ -250,6 +251,7 @@ __global__ void __launch_bounds__(kCorrThreads, 1) corr_detect_kernel(const __gr
             for (int it = 0; it < kchunks; ++it) {
                 const int s = it % kCorrStages;
                 mbar_wait(&sm.full[s], (it / kCorrStages) & 1);
+                if (p.dbg_stages && blockIdx.x < 8 && it < 128) p.dbg_stages[blockIdx.x * 256 + 128 + it] = clock64();
                 // The stage's bytes are in smem (written through the generic
                 // proxy by cp.async); order them before the async-proxy MMA reads.
                 if (!(p.exp_flags & 1)) fence_proxy_async_smem();

@@ -68,6 +68,7 @@ struct DetectParams {
     int32_t tile_m;     // images per decode tile (<= 128 TMEM lanes); set by the launcher
     int32_t exp_flags;  // experiment hooks (bit 0: skip the consumer proxy fence)
     unsigned long long* dbg_times;  // nullable: per-CTA phase timestamps (globaltimer ns), 8 per CTA
+    long long* dbg_stages;          // nullable: CTAs 0-7, [cta][2][128] clock64 at producer issue / MMA full
     uint64_t key_cw, key_msg;
     const int8_t* patterns;   // [64][K_pad] s8, rows >= nbits zero
     const int32_t* colsum;    // [64] sum_px P_i[px]
