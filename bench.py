@@ -343,15 +343,18 @@ def main():
         pass
 
     # e2e through the public host API: pinned host images -> host records.
-    host_pool = torch.empty((POOL, H, W, 3), dtype=torch.uint8, pin_memory=True)
-    host_pool.copy_(pool)
+    # 8,192 pinned host images per rank (1.6 GB; 8 ranks stay well inside host RAM)
+    host_pool = torch.empty((POOL // 2, H, W, 3), dtype=torch.uint8, pin_memory=True)
+    host_pool.copy_(pool[:POOL // 2])
     # records land in pinned host memory (a pageable buffer would be registered per call)
     recs_pin = torch.empty((BATCH, q.RECORD_DTYPE.itemsize), dtype=torch.uint8, pin_memory=True)
     recs_h = recs_pin.numpy().view(q.RECORD_DTYPE).reshape(-1)
     plan = ([1, 2, 1], [BATCH // 2] * 3)
 
+    nb_host = (POOL // 2) // BATCH
+
     def e2e_step(i, mode):
-        b = i % nb
+        b = i % nb_host
         first = (i * world + rank) * BATCH
         ptr = host_pool[b * BATCH].data_ptr()
         _, st = ctx.detect_host(None, first, plan=plan, mode=mode, out=recs_h, ptr=ptr, shape=(BATCH, H, W))
