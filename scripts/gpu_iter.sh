@@ -1,2 +1,2 @@
 cd $GRAFT_REPO_ROOT
-QRM_DEBUG_STAGES=1 timeout 300 python scripts/dbg_corr.py 2>&1 | grep "qrm stages" | head -12
+timeout 900 python -m pytest tests/test_gpu_rs.py -x -q -m gpu -k "10m" --durations=5 2>&1 | tail -8

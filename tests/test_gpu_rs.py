@@ -160,3 +160,22 @@ def test_stress_10m_properties(qrm, cuda, orc):
         assert np.array_equal(ne[sl].cpu().numpy(), ne_o)
         okm = ne_o >= 0
         assert np.array_equal(cw[sl].cpu().numpy().view(np.uint64)[okm], cw_o[okm])
+
+
+def test_stress_10m_bit_exact_vs_reference(qrm, cuda, ref):
+    """configs[3] in full: all 10M stress words (e = 0..t plus ~10% beyond t)
+    through both device decoders equal the compiled reference's bw_decode
+    (rs.cpp:188-196) on every word — codeword, errors_corrected and failure."""
+    import os
+    code = qrm.resolve_profile("gf16-15-12")
+    N = 10_000_000
+    msg, words, ne_true = qrm.rs_stress_words(code, 2026, N)
+    w_h = words.cpu().numpy().view(np.uint64)
+    cw_r, ne_r, _ = ref.bw_decode_packed(code.m, code.n, code.k, w_h, threads=os.cpu_count() or 1)
+    ok = ne_r >= 0
+    assert 0.85 < ok.mean() < 0.97  # the >t share mostly fails, as bounded-distance decoding must
+    for algo in (1, 2):
+        cw, ne = qrm.bw_decode_packed(code, words, algo=algo)
+        ne_g = ne.cpu().numpy()
+        assert np.array_equal(ne_g, ne_r), algo
+        assert np.array_equal(cw.cpu().numpy().view(np.uint64)[ok], cw_r[ok]), algo
