@@ -92,6 +92,17 @@ namespace {
 
 cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
+// Runs f when the scope ends, on success and on every early error return.
+template <typename F>
+struct OnExit {
+    F f;
+    ~OnExit() { f(); }
+};
+template <typename F>
+OnExit<F> on_exit(F f) {
+    return OnExit<F>{f};
+}
+
 int64_t now_ns() {
     return std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now().time_since_epoch())
         .count();
@@ -634,6 +645,17 @@ QRM_EXPORT qrm_status qrm_detect_host(qrm_ctx* c, const uint8_t* images, int64_t
     // Host buffers must be page-locked and mapped; register them for the call if not.
     const int64_t in_bytes = (count - 1) * stride + static_cast<int64_t>(w) * h * 3;
     bool reg_in = false, reg_out = false;
+    std::vector<cudaEvent_t> ev;
+    int nstreams_used = 0;
+    // Every exit path (errors included) drains the streams this call used
+    // before it releases the events and unregisters the caller's buffers.
+    auto cleanup = on_exit([&] {
+        for (int i = 0; i < nstreams_used; ++i) cudaStreamSynchronize(c->streams[i]);
+        for (auto e : ev)
+            if (e) cudaEventDestroy(e);
+        if (reg_in) cudaHostUnregister(const_cast<uint8_t*>(images));
+        if (reg_out) cudaHostUnregister(out);
+    });
     cudaPointerAttributes attr{};
     if (cudaPointerGetAttributes(&attr, images) != cudaSuccess || attr.type != cudaMemoryTypeHost) {
         cudaGetLastError();
@@ -688,7 +710,8 @@ QRM_EXPORT qrm_status qrm_detect_host(qrm_ctx* c, const uint8_t* images, int64_t
         }
     }
 
-    std::vector<cudaEvent_t> ev(4 * nstreams + 3 * nmb);
+    nstreams_used = nstreams;
+    ev.assign(4 * nstreams + 3 * nmb, nullptr);
     for (auto& e : ev) QRM_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     size_t evi = 0;
     std::vector<cudaEvent_t> slot_free(s1, nullptr);  // decode slot j reusable after its last finish
@@ -813,9 +836,6 @@ QRM_EXPORT qrm_status qrm_detect_host(qrm_ctx* c, const uint8_t* images, int64_t
         slot_free[slot] = e_done;
     }
     for (int i = 0; i < nstreams; ++i) QRM_CUDA(cudaStreamSynchronize(c->streams[i]));
-    for (auto& e : ev) cudaEventDestroy(e);
-    if (reg_in) cudaHostUnregister(const_cast<uint8_t*>(images));
-    if (reg_out) cudaHostUnregister(out);
     if (stats) {
         stats->wall_ms = static_cast<double>(now_ns() - t0) / 1e6;
         stats->h2d_bytes = h2d;
@@ -1445,6 +1465,13 @@ QRM_EXPORT qrm_status qrm_warmup_profile_mode(qrm_ctx* c, const uint8_t* images,
     geometry(w, h, up, sw, sh, xo, yo);
     const uint8_t* mapped = nullptr;
     bool reg = false;
+    cudaEvent_t a = nullptr, b = nullptr;
+    auto cleanup = on_exit([&] {
+        cudaDeviceSynchronize();  // nothing of this call may still read the caller's buffer
+        if (a) cudaEventDestroy(a);
+        if (b) cudaEventDestroy(b);
+        if (reg) cudaHostUnregister(const_cast<uint8_t*>(images));
+    });
     if (mode == 0) {
         cudaPointerAttributes attr{};
         if (cudaPointerGetAttributes(&attr, images) != cudaSuccess || attr.type != cudaMemoryTypeHost) {
@@ -1455,14 +1482,11 @@ QRM_EXPORT qrm_status qrm_warmup_profile_mode(qrm_ctx* c, const uint8_t* images,
         }
         QRM_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(const_cast<uint8_t**>(&mapped)),
                                           const_cast<uint8_t*>(images), 0));
-        if (!direct_ok(c, mapped, w, h, stride) || (3 * c->l) % 16 != 0) {
-            if (reg) cudaHostUnregister(const_cast<uint8_t*>(images));
+        if (!direct_ok(c, mapped, w, h, stride) || (3 * c->l) % 16 != 0)
             return fail(QRM_INVALID_INPUT, "window fetch needs 16-B aligned windows (use mode 1)");
-        }
     }
     std::vector<qrm_record> host(b0);
     cudaStream_t st = nullptr;
-    cudaEvent_t a, b;
     QRM_CUDA(cudaEventCreate(&a));
     QRM_CUDA(cudaEventCreate(&b));
     auto timed = [&](auto&& body) -> double {
@@ -1506,9 +1530,6 @@ QRM_EXPORT qrm_status qrm_warmup_profile_mode(qrm_ctx* c, const uint8_t* images,
             cudaMemcpyAsync(host.data(), c->d_records, sizeof(qrm_record) * b0, cudaMemcpyDeviceToHost, st);
         }));
     }
-    cudaEventDestroy(a);
-    cudaEventDestroy(b);
-    if (reg) cudaHostUnregister(const_cast<uint8_t*>(images));
     auto med = [](std::vector<double> v) {
         std::sort(v.begin(), v.end());
         double x = v[v.size() / 2];
