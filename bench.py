@@ -410,6 +410,30 @@ def main():
     except Exception as exc:
         hidden = {"unavailable": str(exc)}
 
+    # North-star item 1: u8 images -> bf16 NHWC tiles (TMA-staged windows), HBM-bound.
+    try:
+        tiles_out = torch.empty((BATCH, 64, 64, 3), dtype=torch.bfloat16, device=dev)
+        for i in range(3):
+            ctx.extract_tiles(pool[(i % nb) * BATCH:(i % nb + 1) * BATCH], first_draw=i * BATCH, out=tiles_out)
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        reps = 20
+        a.record(stream)
+        for i in range(reps):
+            ctx.extract_tiles(pool[(i % nb) * BATCH:(i % nb + 1) * BATCH], first_draw=i * BATCH, out=tiles_out)
+        b.record(stream)
+        torch.cuda.synchronize()
+        tms = max_over_ranks(a.elapsed_time(b) / reps)
+        tb = BATCH * (ctx.window_bytes + 2 * ctx.window_bytes)
+        tile_extract = {"tiles_per_s": world * BATCH / (tms / 1e3), "ms_per_batch": tms, "batch": BATCH,
+                        "out": "bf16 NHWC [B, 64, 64, 3]",
+                        "roofline": {"bound": "hbm", "achieved": tb / (tms / 1e3) / 1e9, "peak": _peaks()[0],
+                                     "unit": "GB/s", "frac": tb / (tms / 1e3) / 1e9 / _peaks()[0],
+                                     "algorithmic_bytes_per_launch": tb}}
+        del tiles_out
+    except Exception as exc:
+        tile_extract = {"unavailable": str(exc)}
+
     try:
         config512 = config512_submetric(q, ctx, cfg, world, rank, max_over_ranks, args.warmup)
     except Exception as exc:
@@ -475,6 +499,7 @@ def main():
             "rs": {"words": args.rs_words, "profile": "gf16-15-12", **rs},
             "learned_extractor": hidden,
             "robustness": robustness,
+            "tile_extract": tile_extract,
             "config_512": config512,
             "cpu_baseline": cpu,
             "clocks": clocks.summary(),

@@ -159,6 +159,16 @@ QRM_EXPORT qrm_status qrm_hidden_detect_device(qrm_ctx* ctx, const uint8_t* imag
                                                int64_t image_stride, uint64_t first_draw, uint64_t weight_seed,
                                                float* logits, qrm_record* out, void* stream);
 
+/* Tile extraction + normalisation (north-star item 1): for each image,
+ * preprocess (transforms.cpp:42-47) -> select_tile (draw first_draw + i,
+ * tiling.cpp:23-47) -> extract_tile (tiling.cpp:62-77) -> normalize
+ * (image.cpp:32-38), emitted as bf16 NHWC [count][64][64][channels]
+ * (channels 3, or 4 with a zero 4th channel for 8-byte pixels) in device
+ * memory: the input a learned decoder's first layer consumes. Needs l = 64. */
+QRM_EXPORT qrm_status qrm_extract_tiles_device(qrm_ctx* ctx, const uint8_t* images, int64_t count, int w, int h,
+                                               int64_t image_stride, uint64_t first_draw, int channels, void* out,
+                                               void* stream);
+
 /* Extractor behind the WatermarkCodec plug-in point (stego.hpp:32-40) used by
  * qrm_detect_device / qrm_detect_host / qrm_detect_ragged:
  *   QRM_EXTRACTOR_SPREAD_SPECTRUM (default): SpreadSpectrumCodec::extract

@@ -27,7 +27,7 @@ LIB_PATH = os.path.join(_HERE, "_lib", "libqrmark_b200.so")
 # Exported symbols of include/qrmark_gpu.h (checked by the CPU test suite).
 ABI_SYMBOLS = (
     "qrm_last_error", "qrm_abi_version", "qrm_device_count", "qrm_ctx_create", "qrm_ctx_destroy", "qrm_ctx_info",
-    "qrm_ctx_set_extractor", "qrm_ppm_read", "qrm_ppm_write", "qrm_ppm_read_batch", "qrm_records_json", "qrm_cache_hits", "qrm_attack_device", "qrm_warmup_profile_mode",
+    "qrm_ctx_set_extractor", "qrm_ppm_read", "qrm_ppm_write", "qrm_ppm_read_batch", "qrm_records_json", "qrm_cache_hits", "qrm_attack_device", "qrm_warmup_profile_mode", "qrm_extract_tiles_device",
     "qrm_detect_device", "qrm_detect_host", "qrm_detect_ragged", "qrm_extract_device", "qrm_preprocess_host",
     "qrm_rs_decode_packed_device", "qrm_rs_decode_symbols_device", "qrm_rs_stress_device", "qrm_rs_encode_packed",
     "qrm_verify_threshold", "qrm_make_corpus_device", "qrm_patterns_device", "qrm_allocate_streams",
@@ -98,6 +98,7 @@ def lib() -> C.CDLL:
         L.qrm_ctx_destroy.argtypes = [vp]
         L.qrm_ctx_info.argtypes = [vp, C.POINTER(u64), C.POINTER(u64), C.POINTER(i32), C.POINTER(i32)]
         L.qrm_ctx_set_extractor.argtypes = [vp, i32, u64]
+        L.qrm_extract_tiles_device.argtypes = [vp, vp, i64, i32, i32, i64, u64, i32, vp, vp]
         L.qrm_attack_device.argtypes = [vp, i64, i32, i32, i64, i32, C.c_double, vp, i64, C.POINTER(i32),
                                         C.POINTER(i32), vp]
         L.qrm_ppm_read.argtypes = [C.c_char_p, vp, i64, C.POINTER(i32), C.POINTER(i32)]
@@ -449,6 +450,18 @@ class DetectionContext:
         _check(lib().qrm_hidden_detect_device(self._h, _ptr(images), B, W, H, images.stride(0), first_draw,
                                               weight_seed, _ptr(lg), _ptr(out), _stream(stream)))
         return lg, out
+
+    def extract_tiles(self, images, first_draw: int = 0, channels: int = 3, out=None, stream=None):
+        """preprocess -> select_tile -> extract_tile -> normalize as bf16 NHWC tiles
+        [B, l, l, channels] on the device (channels 4: zero-padded)."""
+        import torch
+        B, H, W, _ = images.shape
+        l = self.cfg.tile_size
+        if out is None:
+            out = torch.empty((B, l, l, channels), dtype=torch.bfloat16, device=images.device)
+        _check(lib().qrm_extract_tiles_device(self._h, _ptr(images), B, W, H, images.stride(0), first_draw, channels,
+                                              _ptr(out), _stream(stream)))
+        return out
 
     def extract_device(self, images, first_draw: int = 0, soft: bool = True, stream=None):
         """SpreadSpectrumCodec::extract + harden on a device batch -> (soft float64 [B, N] or None, raw int64 [B])."""

@@ -41,6 +41,7 @@ cudaError_t launch_gather_windows(const GatherDesc* descs, int64_t count, int l,
 cudaError_t launch_fetch_windows(const WindowSource& src, int64_t count, int K, uint8_t* out, int sm_count,
                                  cudaStream_t st);
 cudaError_t launch_attack_pixels(const AttackParams& p, cudaStream_t st);
+cudaError_t launch_tile_bf16(const CUtensorMap& tmap, const TileBf16Params& p, int sm_count, cudaStream_t st);
 cudaError_t launch_attack_jpeg(const AttackParams& p, cudaStream_t st);
 cudaError_t launch_attack_resample(const AttackParams& p, cudaStream_t st);
 cudaError_t launch_rs_packed(const RsTables* tab, int m, int r, int t, int algo, const uint64_t* words,
@@ -977,7 +978,7 @@ QRM_EXPORT qrm_status qrm_make_corpus_device(const qrm_config* cfg, uint64_t fir
 namespace {
 
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda).
-qrm_status encode_act_tmap(CUtensorMap* map, CUtensorMap* store_map, void* base, int64_t tiles) {
+qrm_status tensor_map_encoder(PFN_cuTensorMapEncodeTiled_v12000* out) {
     static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
     if (!encode) {
         cudaDriverEntryPointQueryResult q;
@@ -986,6 +987,13 @@ qrm_status encode_act_tmap(CUtensorMap* map, CUtensorMap* store_map, void* base,
         if (q != cudaDriverEntryPointSuccess || !fn) return fail(QRM_CUDA_ERROR, "cuTensorMapEncodeTiled unavailable");
         encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
     }
+    *out = encode;
+    return QRM_OK;
+}
+
+qrm_status encode_act_tmap(CUtensorMap* map, CUtensorMap* store_map, void* base, int64_t tiles) {
+    PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+    if (qrm_status s = tensor_map_encoder(&encode); s != QRM_OK) return s;
     // activations NHWC bf16 [T][64 y][64 x][64 c]; box = 4 rows of 64 pixels
     const cuuint64_t dims[4] = {64, 64, 64, static_cast<cuuint64_t>(tiles)};
     const cuuint64_t strides[3] = {64 * 2, 64 * 64 * 2, 64 * 64 * 64 * 2};
@@ -1131,6 +1139,43 @@ QRM_EXPORT qrm_status qrm_hidden_detect_device(qrm_ctx* c, const uint8_t* images
         s = hidden_run(c, W, src, count, out, logits, st);
     c->conv_seed = keep;
     return s;
+}
+
+QRM_EXPORT qrm_status qrm_extract_tiles_device(qrm_ctx* c, const uint8_t* images, int64_t count, int w, int h,
+                                               int64_t stride, uint64_t first_draw, int channels, void* out,
+                                               void* stream) {
+    // preprocess -> select_tile -> extract_tile -> normalize as bf16 NHWC tiles.
+    qrm_status s = check_uniform(c, images, count, w, h, stride);
+    if (s != QRM_OK) return s;
+    if (c->l != 64) return fail(QRM_INVALID_INPUT, "bf16 tile extraction is built for 64x64 tiles");
+    if (channels != 3 && channels != 4) return fail(QRM_INVALID_INPUT, "channels must be 3 or 4");
+    if (count > 0 && !out) return fail(QRM_INVALID_INPUT, "null output buffer");
+    if (count >= (int64_t{1} << 31)) return fail(QRM_INVALID_INPUT, "too many tiles for one launch");
+    if ((s = set_device(c->device)) != QRM_OK) return s;
+    if (count == 0) return QRM_OK;
+    cudaStream_t st = as_stream(stream);
+    Workspace& W = c->ws[0];
+    WindowSource src;
+    if ((s = window_source(c, W, images, count, w, h, stride, first_draw, st, src)) != QRM_OK) return s;
+    PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+    if ((s = tensor_map_encoder(&encode)) != QRM_OK) return s;
+    // u8 images viewed as [count][rows][row bytes]; box = one 64 x 192-B window
+    const bool direct = src.direct != 0;
+    const cuuint64_t dims[3] = {static_cast<cuuint64_t>(direct ? w * 3 : 192), static_cast<cuuint64_t>(direct ? h : 64),
+                                static_cast<cuuint64_t>(count)};
+    const cuuint64_t strides[2] = {static_cast<cuuint64_t>(direct ? w * 3 : 192),
+                                   static_cast<cuuint64_t>(direct ? stride : c->K)};
+    const cuuint32_t box[3] = {192, 64, 1};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    CUtensorMap map;
+    const CUresult r = encode(&map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<uint8_t*>(src.base), dims, strides,
+                              box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                              // 64-B fills: a 192-B row at a 64-B offset, no over-read
+                              CU_TENSOR_MAP_L2_PROMOTION_L2_64B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(QRM_CUDA_ERROR, "cuTensorMapEncodeTiled (tiles) failed (" + std::to_string(r) + ")");
+    TileBf16Params p{src, count, c->K, channels, static_cast<uint16_t*>(out)};
+    QRM_LAUNCH(launch_tile_bf16(map, p, c->sms, st));
+    return QRM_OK;
 }
 
 QRM_EXPORT qrm_status qrm_ctx_set_extractor(qrm_ctx* c, int kind, uint64_t weight_seed) {

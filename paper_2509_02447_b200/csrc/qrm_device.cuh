@@ -207,6 +207,15 @@ QRM_D void tma_load_4d(uint32_t dst_smem, const void* tmap, int c0, int c1, int 
         : "memory");
 }
 
+// 3-D TMA tile load global -> shared, completion on an mbarrier (tx bytes).
+QRM_D void tma_load_3d(uint32_t dst_smem, const void* tmap, int c0, int c1, int c2, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+        "[%5];" ::"r"(dst_smem),
+        "l"(tmap), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+        : "memory");
+}
+
 // TMA tensor store shared -> global (bulk-group completion).
 QRM_D void tma_store_2d(const void* tmap, uint32_t src_smem, int c0, int c1) {
     asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(tmap),

@@ -101,4 +101,14 @@ struct AttackParams {
     double dct_c0;            // sqrt(0.125)
 };
 
+
+// Tile extraction + normalisation into bf16 NHWC (north-star item 1).
+struct TileBf16Params {
+    WindowSource src;  // tile origins (direct) or contiguous staged windows
+    int64_t count;
+    int32_t K;         // 3 l^2
+    int32_t channels;  // 3 or 4 output channels (4: zero-padded, 8-byte pixels)
+    uint16_t* out;     // [count][l][l][channels] bf16
+};
+
 }  // namespace qrm

@@ -1,0 +1,94 @@
+// Tile extraction and normalisation into bf16 NHWC tiles (north-star item 1):
+// preprocess (transforms.cpp:42-47; a centre crop at >= 256 px) -> select_tile
+// (tiling.cpp:23-47) -> extract_tile (tiling.cpp:62-77) -> normalize
+// (image.cpp:32-38: float(v / 127.5 - 1)), emitted as bf16 (round to nearest
+// even) for a learned decoder's first layer.
+//
+// tile_bf16_kernel: persistent CTAs; one elected thread streams each tile's
+// 64 rows x 192 B window into shared memory with a single 3-D TMA box
+// (images viewed as [count][rows][row bytes], the box placed at the tile's
+// origin), double buffered so the next window lands while this one is
+// converted. All threads then map bytes through a 256-entry bf16 table and
+// write the tile's contiguous 24 KB (or 32 KB padded to 4 channels) with 16-B
+// stores. HBM-bound: 12,288 B read + 24,576 B written per tile.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include "qrm_device.cuh"
+#include "qrm_types.h"
+
+namespace qrm {
+
+constexpr int kTbThreads = 256;
+constexpr int kTbRow = 192;             // 64 px x 3 B
+constexpr int kTbWin = 64 * kTbRow;     // 12,288 B
+
+__global__ void __launch_bounds__(kTbThreads) tile_bf16_kernel(const __grid_constant__ CUtensorMap tmap,
+                                                               const __grid_constant__ TileBf16Params p) {
+    __shared__ __align__(128) uint8_t win[2][kTbWin];
+    __shared__ uint16_t lut[256];
+    __shared__ __align__(8) uint64_t full[2];
+    const int tid = threadIdx.x;
+    for (int v = tid; v < 256; v += kTbThreads) {
+        const float f = __double2float_rn(__dsub_rn(__ddiv_rn(static_cast<double>(v), 127.5), 1.0));
+        lut[v] = __bfloat16_as_ushort(__float2bfloat16_rn(f));
+    }
+    if (tid == 0) {
+        mbar_init(&full[0], 1);
+        mbar_init(&full[1], 1);
+        mbar_fence_init();
+    }
+    __syncthreads();
+    auto issue = [&](int64_t t, int buf) {
+        int x0 = 0, y0 = 0;
+        if (p.src.direct) {
+            int tx, ty;
+            select_tile(kWorkingSize, kWorkingSize, p.src.l, p.src.strategy, p.src.tile_seed,
+                        p.src.first_draw + static_cast<uint64_t>(t), tx, ty);
+            x0 = (p.src.x_off + tx) * 3;
+            y0 = p.src.y_off + ty;
+        }
+        mbar_arrive_expect_tx(&full[buf], kTbWin);
+        tma_load_3d(smem_u32(win[buf]), &tmap, x0, y0, static_cast<int>(t), &full[buf]);
+    };
+    int64_t t = blockIdx.x;
+    if (tid == 0 && t < p.count) issue(t, 0);
+    for (int i = 0; t < p.count; t += gridDim.x, ++i) {
+        const int buf = i & 1;
+        // the other buffer was fully consumed before the previous iteration's barrier
+        if (tid == 0 && t + gridDim.x < p.count) issue(t + gridDim.x, buf ^ 1);
+        mbar_wait(&full[buf], (i >> 1) & 1);
+        const uint8_t* w = win[buf];
+        if (p.channels == 4) {
+            // 2 pixels (6 bytes -> 16 B) per 16-B store; 2048 stores per tile
+            uint4* dst = reinterpret_cast<uint4*>(p.out + t * (64 * 64 * 4));
+            for (int j = tid; j < 64 * 64 / 2; j += kTbThreads) {
+                const uint8_t* s = w + j * 6;
+                dst[j] = make_uint4(lut[s[0]] | (static_cast<uint32_t>(lut[s[1]]) << 16), lut[s[2]],
+                                    lut[s[3]] | (static_cast<uint32_t>(lut[s[4]]) << 16), lut[s[5]]);
+            }
+        } else {
+            // 8 bytes -> one 16-B store; 1536 stores per tile
+            uint4* dst = reinterpret_cast<uint4*>(p.out + t * (64 * 64 * 3));
+            for (int j = tid; j < kTbWin / 8; j += kTbThreads) {
+                const uint8_t* s = w + j * 8;
+                dst[j] = make_uint4(lut[s[0]] | (static_cast<uint32_t>(lut[s[1]]) << 16),
+                                    lut[s[2]] | (static_cast<uint32_t>(lut[s[3]]) << 16),
+                                    lut[s[4]] | (static_cast<uint32_t>(lut[s[5]]) << 16),
+                                    lut[s[6]] | (static_cast<uint32_t>(lut[s[7]]) << 16));
+            }
+        }
+        __syncthreads();  // every thread is done with win[buf] before it is refilled
+    }
+}
+
+cudaError_t launch_tile_bf16(const CUtensorMap& tmap, const TileBf16Params& p, int sm_count, cudaStream_t st) {
+    if (p.count <= 0) return cudaSuccess;
+    int64_t grid = static_cast<int64_t>(sm_count > 0 ? sm_count : 148) * 8;
+    if (grid > p.count) grid = p.count;
+    tile_bf16_kernel<<<static_cast<unsigned>(grid), kTbThreads, 0, st>>>(tmap, p);
+    return cudaGetLastError();
+}
+
+}  // namespace qrm

@@ -187,3 +187,26 @@ def test_host_pipeline_equals_device(qrm, cuda, cfg, mode):
         rec, st = ctx.detect_host(host, first_draw=50, plan=([2, 3, 2], [128, 128, 128]), mode=mode)
     assert np.array_equal(rec.view(np.uint8), dev.view(np.uint8))
     assert st["minibatches"] == 8
+
+
+@pytest.mark.gpu
+def test_bf16_tiles_match_reference_preprocess(qrm, cuda, ref):
+    """North-star item 1: u8 images -> bf16 NHWC tiles equals the reference's
+    preprocess + select_tile + extract_tile (float) rounded to bf16, for the
+    direct TMA path (256^2, 512^2) and the staged path (upscaled 200x150)."""
+    import dataclasses
+    for strategy in ("random_grid", "random"):
+        cfg = dataclasses.replace(qrm.DetectionConfig(), tile_strategy=strategy)
+        for (h, w) in [(256, 256), (512, 512), (150, 200)]:
+            imgs = qrm.make_corpus(cfg, 1000, 6, w, h)
+            with qrm.DetectionContext(cfg) as ctx:
+                t3 = ctx.extract_tiles(imgs, first_draw=9, channels=3)
+                t4 = ctx.extract_tiles(imgs, first_draw=9, channels=4)
+            cuda.cuda.synchronize()
+            assert bool((t4[..., 3] == 0).all()) and bool((t4[..., :3] == t3).all())
+            host = imgs.cpu().numpy()
+            for i in range(host.shape[0]):
+                pre = ref.preprocess(host[i])
+                x, y = ref.select_tile(256, 256, 64, strategy, 0, 9 + i)
+                want = cuda.tensor(pre[y:y + 64, x:x + 64]).to(cuda.bfloat16)
+                assert bool((t3[i].cpu() == want).all()), (strategy, h, w, i)
