@@ -1,3 +1,7 @@
 cd $GRAFT_REPO_ROOT
-timeout 600 python -m pytest tests/test_hidden.py tests/test_cpp_dropin.py -x -q -m gpu 2>&1 | tail -3
-for i in 1 2; do python scripts/bench_hidden.py 4096; done
+( time timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err ) 2> gpurun_out/bench_time.txt
+tail -3 gpurun_out/bench.err; grep real gpurun_out/bench_time.txt
+python -c "
+import json; d = json.load(open('gpurun_out/bench.json'))
+for k in ('value','e2e','job_1m','tile_extract','config_512'): print(k, json.dumps(d.get(k))[:400])
+"
