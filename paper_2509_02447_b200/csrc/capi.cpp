@@ -1015,12 +1015,13 @@ qrm_status encode_act_tmap(CUtensorMap* map, CUtensorMap* store_map, void* base,
     return QRM_OK;
 }
 
-// One 64->64 conv layer: single-CTA kernel; QRM_CONV_PAIR=1 selects the CTA-pair
-// (cta_group::2) variant (correct, but measured 11.1 vs 9.8 ms per 4096 tiles).
+// One 64->64 conv layer: the CTA-pair kernel (cta_group::2, M = 256; 237 us per
+// 1024 tiles against 285 us for the single-CTA kernel); QRM_CONV_PAIR=0 selects
+// the single-CTA variant.
 cudaError_t conv64_layer(const CUtensorMap& tmap, const CUtensorMap& tmap_out, const HiddenLayerParams& p, int sms,
                          cudaStream_t st) {
     const char* e = getenv("QRM_CONV_PAIR");
-    const bool pair = e && e[0] == '1';
+    const bool pair = !(e && e[0] == '0');
     return pair ? launch_conv64_pair(tmap, tmap_out, p, sms, st) : launch_conv64(tmap, tmap_out, p, sms, st);
 }
 

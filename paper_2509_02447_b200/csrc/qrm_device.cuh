@@ -372,12 +372,16 @@ QRM_D void umma_commit_pair_mc(uint64_t* bar, uint16_t mask) {
         : "memory");
 }
 // Arrive on an mbarrier of another CTA of the cluster (address from map_to_rank).
+// Default semantics (.release at CTA scope), as CUTLASS's ClusterBarrier does:
+// a .release.cluster arrive waits for all of the thread's outstanding writes
+// (the epilogue's output stores) to reach cluster scope, and measured as half
+// of the pair kernel's warp stalls. The barriers only order TMEM/smem reuse,
+// which tcgen05.wait::ld / the fences before the arrive already cover.
 QRM_D void mbar_arrive_cluster(uint32_t cluster_addr) {
-    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+    asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
 QRM_D void mbar_arrive_expect_tx_cluster(uint32_t cluster_addr, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.release.cluster.shared::cluster.b64 _, [%0], %1;" ::"r"(cluster_addr),
-                 "r"(bytes)
+    asm volatile("mbarrier.arrive.expect_tx.shared::cluster.b64 _, [%0], %1;" ::"r"(cluster_addr), "r"(bytes)
                  : "memory");
 }
 // 4-D TMA load into this CTA's smem whose completion is signalled on a barrier

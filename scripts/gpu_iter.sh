@@ -1,7 +1,4 @@
 cd $GRAFT_REPO_ROOT
-( time timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err ) 2> gpurun_out/bench_time.txt
-tail -3 gpurun_out/bench.err; grep real gpurun_out/bench_time.txt
-python -c "
-import json; d = json.load(open('gpurun_out/bench.json'))
-for k in ('value','e2e','job_1m','tile_extract','config_512'): print(k, json.dumps(d.get(k))[:400])
-"
+timeout 600 python -m pytest tests/test_hidden.py tests/test_cpp_dropin.py -x -q -m gpu 2>&1 | tail -2
+for i in 1 2 3; do python scripts/bench_hidden.py 4096; done
+ncu --set full --import-source on --clock-control none -k regex:conv64 -s 10 -c 1 -o gpurun_out/conv64pair2 python scripts/bench_hidden.py 1024 > /dev/null 2>&1; ls gpurun_out/conv64pair2*
