@@ -182,7 +182,9 @@ def hidden_submetric(ctx, pool, world, max_over_ranks, stream, batch=BATCH, reps
         cfg = dataclasses.replace(ctx.cfg, extractor="conv")
         recs_pin = torch.empty((batch, q.RECORD_DTYPE.itemsize), dtype=torch.uint8, pin_memory=True)
         recs = recs_pin.numpy().view(q.RECORD_DTYPE).reshape(-1)
-        plan = ([1, 1, 1], [batch // 2] * 3)
+        # one mini-batch: the conv layers' fixed costs amortise better than the
+        # fetch/decode overlap smaller mini-batches buy (scripts/e2e_conv.py)
+        plan = ([1, 1, 1], [batch] * 3)
         H, W = host_pool.shape[1], host_pool.shape[2]
         with q.DetectionContext(cfg, device=ctx.device) as cctx:
             def one(i):
