@@ -138,6 +138,7 @@ __global__ void __launch_bounds__(kCorrThreads, 1) corr_detect_kernel(const __gr
         mbar_init(&sm.accum_full, 1);
         mbar_fence_init();
     }
+    griddep_launch_dependents();  // the completion kernel may launch; it waits for this grid
     if (tid < kCorrN) sm.thr[tid] = 255 * __ldg(p.colsum + tid);
     if (p.fuse_t1) rs_stage_tables(sm.rs, p.rs, tid, kCorrThreads);
     tc_fence_before();
@@ -230,6 +231,7 @@ __global__ void __launch_bounds__(kCorrThreads, 1) corr_detect_kernel(const __gr
 
         const int row = warp * 32 + lane;
         if (S == 1) {
+            griddep_wait();  // the previous completion kernel is done with records / the pending list
             const int64_t img = m0 + row;
             if (row < tile_m && img < p.count) finish_image(p, sm, img, acc);
             dbg_mark(p, 5, tid);
@@ -272,6 +274,7 @@ __global__ void __launch_bounds__(kCorrThreads, 1) corr_detect_kernel(const __gr
         cluster_sync_all();  // every partial row has landed in its owner's smem
         dbg_mark(p, 6, tid);
         if (tid < rows_per) {
+            griddep_wait();  // the previous completion kernel is done with records / the pending list
             uint32_t acc[kCorrN];
 #pragma unroll
             for (int i = 0; i < kCorrN; ++i) acc[i] = 0;
@@ -309,8 +312,12 @@ static cudaLaunchConfig_t corr_config(unsigned grid, unsigned S, cudaStream_t st
     attr[0].val.clusterDim.x = S;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
+    // programmatic dependent launch: the prologue and streaming may overlap the
+    // previous kernel; the epilogue griddep_wait()s before writing outputs
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = 2;
     return cfg;
 }
 
@@ -318,7 +325,7 @@ static cudaLaunchConfig_t corr_config(unsigned grid, unsigned S, cudaStream_t st
 static int max_active_clusters(unsigned S, int sms) {
     static int cache[9] = {0};
     if (cache[S] == 0) {
-        cudaLaunchAttribute attr[1];
+        cudaLaunchAttribute attr[2];
         cudaLaunchConfig_t cfg = corr_config(S * 64, S, nullptr, attr);
         int n = 0;
         if (cudaOccupancyMaxActiveClusters(&n, corr_detect_kernel, &cfg) != cudaSuccess || n <= 0) {
@@ -360,7 +367,7 @@ cudaError_t launch_corr_detect(const DetectParams& p_in, int sm_count, cudaStrea
     tiles = (p_in.count + tile_m - 1) / tile_m;
     DetectParams p = p_in;
     p.tile_m = static_cast<int32_t>(tile_m);
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     cudaLaunchConfig_t cfg = corr_config(static_cast<unsigned>(tiles) * S, S, st, attr);
     return cudaLaunchKernelEx(&cfg, corr_detect_kernel, p);
 }

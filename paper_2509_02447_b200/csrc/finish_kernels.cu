@@ -37,6 +37,8 @@ template <int TMAX>
 __global__ void __launch_bounds__(256) detect_finish_kernel(const __grid_constant__ DetectParams p) {
     __shared__ RsSmem T;
     __shared__ int npend_s;
+    griddep_wait();               // the decode grid's records and pending list are complete
+    griddep_launch_dependents();  // the next decode may start its prologue
     if (threadIdx.x == 0) npend_s = *reinterpret_cast<volatile int32_t*>(p.pending_count);
     __syncthreads();
     const int npend = npend_s;
@@ -207,12 +209,21 @@ cudaError_t launch_fetch_windows(const WindowSource& src, int64_t count, int K, 
 }
 
 cudaError_t launch_detect_finish(const DetectParams& p, int tmax, int sm_count, cudaStream_t st) {
-    const int blocks = sm_count > 0 ? sm_count : 148;
-    if (tmax <= 1) detect_finish_kernel<1><<<blocks, 256, 0, st>>>(p);
-    else if (tmax <= 2) detect_finish_kernel<2><<<blocks, 256, 0, st>>>(p);
-    else if (tmax <= 4) detect_finish_kernel<4><<<blocks, 256, 0, st>>>(p);
-    else detect_finish_kernel<8><<<blocks, 256, 0, st>>>(p);
-    return cudaGetLastError();
+    // Programmatic dependent launch: the completion kernel's launch overlaps the
+    // decode kernel's tail; it griddep_wait()s before reading the decode's output.
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(sm_count > 0 ? sm_count : 148);
+    cfg.blockDim = dim3(256);
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (tmax <= 1) return cudaLaunchKernelEx(&cfg, detect_finish_kernel<1>, p);
+    if (tmax <= 2) return cudaLaunchKernelEx(&cfg, detect_finish_kernel<2>, p);
+    if (tmax <= 4) return cudaLaunchKernelEx(&cfg, detect_finish_kernel<4>, p);
+    return cudaLaunchKernelEx(&cfg, detect_finish_kernel<8>, p);
 }
 
 cudaError_t launch_gather_windows(const GatherDesc* descs, int64_t count, int l, uint8_t* out, cudaStream_t st) {

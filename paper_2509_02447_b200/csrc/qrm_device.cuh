@@ -305,6 +305,14 @@ QRM_HD uint32_t idesc_tf32_f32(int M, int N) {
            (static_cast<uint32_t>(M >> 4) << 24);
 }
 
+// ------------------------------------------- programmatic dependent launch ----
+// The next kernel in the stream may begin launching (its prologue overlaps
+// this kernel's tail); it must griddep_wait() before touching our outputs.
+QRM_D void griddep_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+// Wait until the previous kernel in the stream has completed and its writes
+// are visible (a no-op when this kernel was not launched with PDL).
+QRM_D void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 // ----------------------------------------------------------- clusters ----
 QRM_D uint32_t cluster_ctarank() {
     uint32_t r;

@@ -1,2 +1,3 @@
 cd $GRAFT_REPO_ROOT
-for d in 0 32 16; do echo "pair dbg=$d"; QRM_HIDDEN_DBG=$d ncu --metrics gpu__time_duration.sum,sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed --clock-control none -k regex:conv64 -s 3 -c 1 python scripts/bench_hidden.py 1024 2>/dev/null | grep -E "duration|tensor"; done
+timeout 900 python -m pytest tests -x -q -m gpu 2>&1 | tail -2
+timeout 600 python bench.py --steps 50 --no-cpu-baseline --rs-words 1000000 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['value'], d['ms_per_step'], d['roofline']['kernel_ms'], d['e2e']['value'])"
