@@ -518,6 +518,9 @@ def main():
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                          "frac": achieved / hbm, "traffic": traffic, "kernel": "corr_detect_kernel",
                          "kernel_ms": kern_ms, "peak_kind": peak_kind,
+                         # back-to-back launches overlap (programmatic dependent launch): the
+                         # window bytes per step over the measured step time
+                         "per_step_gbs": alg_bytes / (ms_step / 1e3) / 1e9,
                          "algorithmic_bytes_per_launch": alg_bytes},
             "rs": {"words": args.rs_words, "profile": "gf16-15-12", **rs},
             "learned_extractor": hidden,

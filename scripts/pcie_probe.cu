@@ -223,6 +223,25 @@ int main() {
         }
         timeit("memcpy_h2d_staged_windows", wbytes, [&] { cudaMemcpyAsync(dst, stage, count * static_cast<size_t>(K), cudaMemcpyHostToDevice); });
     }
+    {   // hybrid: half the windows by zero-copy gather, half by DMA of a pre-gathered pinned buffer, concurrently
+        uint8_t* stage2;
+        CK(cudaHostAlloc(&stage2, static_cast<size_t>(count) * K, cudaHostAllocDefault));
+        cudaStream_t s1, s2;
+        CK(cudaStreamCreateWithFlags(&s1, cudaStreamNonBlocking));
+        CK(cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking));
+        for (double frac : {0.5, 0.6, 0.7, 0.8}) {
+            const int na = static_cast<int>(count * frac);
+            char name[64];
+            snprintf(name, sizeof name, "hybrid_zero_copy_%.1f_plus_dma", frac);
+            timeit(name, wbytes, [&] {
+                gather16<4><<<148 * 2, 256, 0, s1>>>(dh, dorg, na, dst);
+                cudaMemcpyAsync(dst + static_cast<size_t>(na) * K, stage2 + static_cast<size_t>(na) * K,
+                                static_cast<size_t>(count - na) * K, cudaMemcpyHostToDevice, s2);
+                cudaStreamSynchronize(s1);
+                cudaStreamSynchronize(s2);
+            });
+        }
+    }
     {   // device-resident images: how fast can the window gather pattern stream from HBM?
         const int dcount = 16384;
         uint8_t *dpool, *dwin;
