@@ -341,6 +341,10 @@ struct DetectionConfig {
     CacheConfig cache;
     ExtractorKind extractor = ExtractorKind::spread_spectrum;
     uint64_t conv_weight_seed = 7;
+    // Additive: devices of the node to shard uniform batches over (contiguous
+    // shards, global draw indices, no collective). Empty: the
+    // context's own device only.
+    std::vector<int> devices;
     static DetectionConfig make(const CodeParams& code, const TileSpec& tile, uint64_t key_seed, double alpha,
                                 BitVec key_message);
 };

@@ -159,6 +159,16 @@ QRM_EXPORT qrm_status qrm_hidden_detect_device(qrm_ctx* ctx, const uint8_t* imag
                                                int64_t image_stride, uint64_t first_draw, uint64_t weight_seed,
                                                float* logits, qrm_record* out, void* stream);
 
+/* qrm_detect_host over several contexts (normally one per device of the node,
+ * SURVEY 8e): context i decodes the contiguous shard [count*i/n,
+ * count*(i+1)/n) with its global draw indices on its own host thread, and its
+ * records land at their global positions in `out`. Images are independent, so
+ * there is no collective; the result equals one qrm_detect_host over the whole
+ * batch. stats (nullable) sums the shards' bytes and launches. */
+QRM_EXPORT qrm_status qrm_detect_host_multi(qrm_ctx* const* ctxs, int nctx, const uint8_t* images, int64_t count,
+                                            int w, int h, int64_t image_stride, uint64_t first_draw, qrm_record* out,
+                                            const qrm_plan* plan, int mode, qrm_host_stats* stats);
+
 /* Tile extraction + normalisation (north-star item 1): for each image,
  * preprocess (transforms.cpp:42-47) -> select_tile (draw first_draw + i,
  * tiling.cpp:23-47) -> extract_tile (tiling.cpp:62-77) -> normalize

@@ -27,7 +27,7 @@ LIB_PATH = os.path.join(_HERE, "_lib", "libqrmark_b200.so")
 # Exported symbols of include/qrmark_gpu.h (checked by the CPU test suite).
 ABI_SYMBOLS = (
     "qrm_last_error", "qrm_abi_version", "qrm_device_count", "qrm_ctx_create", "qrm_ctx_destroy", "qrm_ctx_info",
-    "qrm_ctx_set_extractor", "qrm_ppm_read", "qrm_ppm_write", "qrm_ppm_read_batch", "qrm_records_json", "qrm_cache_hits", "qrm_attack_device", "qrm_warmup_profile_mode", "qrm_extract_tiles_device",
+    "qrm_ctx_set_extractor", "qrm_ppm_read", "qrm_ppm_write", "qrm_ppm_read_batch", "qrm_records_json", "qrm_cache_hits", "qrm_attack_device", "qrm_warmup_profile_mode", "qrm_extract_tiles_device", "qrm_detect_host_multi",
     "qrm_detect_device", "qrm_detect_host", "qrm_detect_ragged", "qrm_extract_device", "qrm_preprocess_host",
     "qrm_rs_decode_packed_device", "qrm_rs_decode_symbols_device", "qrm_rs_stress_device", "qrm_rs_encode_packed",
     "qrm_verify_threshold", "qrm_make_corpus_device", "qrm_patterns_device", "qrm_allocate_streams",
@@ -98,6 +98,8 @@ def lib() -> C.CDLL:
         L.qrm_ctx_destroy.argtypes = [vp]
         L.qrm_ctx_info.argtypes = [vp, C.POINTER(u64), C.POINTER(u64), C.POINTER(i32), C.POINTER(i32)]
         L.qrm_ctx_set_extractor.argtypes = [vp, i32, u64]
+        L.qrm_detect_host_multi.argtypes = [C.POINTER(vp), i32, vp, i64, i32, i32, i64, u64, vp, C.POINTER(_Plan), i32,
+                                            C.POINTER(_HostStats)]
         L.qrm_extract_tiles_device.argtypes = [vp, vp, i64, i32, i32, i64, u64, i32, vp, vp]
         L.qrm_attack_device.argtypes = [vp, i64, i32, i32, i64, i32, C.c_double, vp, i64, C.POINTER(i32),
                                         C.POINTER(i32), vp]
@@ -531,6 +533,22 @@ class DetectionContext:
         _check(lib().qrm_warmup_profile_mode(self._h, p, B, W, H, H * W * 3, iters, b0, mode, t.ctypes.data,
                                              m.ctypes.data))
         return t, m
+
+
+def detect_host_multi(contexts, images: np.ndarray, first_draw: int = 0, plan=None, mode: int = 0, out=None):
+    """qrm_detect_host_multi: one contiguous shard per context (normally one per GPU),
+    each on its own host thread, records at their global positions -> (records, stats)."""
+    images = np.ascontiguousarray(images, dtype=np.uint8)
+    B, H, W, _ = images.shape
+    if out is None:
+        out = np.zeros(B, dtype=RECORD_DTYPE)
+    hs = (C.c_void_p * len(contexts))(*[c._h.value if hasattr(c._h, "value") else c._h for c in contexts])
+    st = _HostStats()
+    pl = _Plan((C.c_int * 3)(*plan[0]), (C.c_int * 3)(*plan[1])) if plan is not None else None
+    _check(lib().qrm_detect_host_multi(hs, len(contexts), images.ctypes.data, B, W, H, H * W * 3, first_draw,
+                                       out.ctypes.data, C.byref(pl) if pl is not None else None, mode, C.byref(st)))
+    return out, {"wall_ms": st.wall_ms, "h2d_bytes": st.h2d_bytes, "d2h_bytes": st.d2h_bytes,
+                 "minibatches": st.minibatches, "kernel_launches": st.kernel_launches}
 
 
 def records_from_device(t) -> np.ndarray:

@@ -22,6 +22,7 @@
 #include <mutex>
 #include <string>
 #include <tuple>
+#include <thread>
 #include <vector>
 
 #include "host_code.hpp"
@@ -843,6 +844,48 @@ QRM_EXPORT qrm_status qrm_detect_host(qrm_ctx* c, const uint8_t* images, int64_t
         stats->d2h_bytes = static_cast<double>(sizeof(qrm_record)) * count;
         stats->minibatches = static_cast<int>(nmb);
         stats->kernel_launches = static_cast<int>(g_launches.load()) - launches0;
+    }
+    return QRM_OK;
+}
+
+QRM_EXPORT qrm_status qrm_detect_host_multi(qrm_ctx* const* ctxs, int nctx, const uint8_t* images, int64_t count,
+                                            int w, int h, int64_t stride, uint64_t first_draw, qrm_record* out,
+                                            const qrm_plan* plan, int mode, qrm_host_stats* stats) {
+    // detect_batch over several devices of one node: images are
+    // independent, so context i takes the contiguous shard
+    // [count*i/n, count*(i+1)/n) with its GLOBAL draw indices, on its own host
+    // thread; records land at their global positions. No collective.
+    if (!ctxs || nctx < 1) return fail(QRM_INVALID_INPUT, "need at least one context");
+    for (int i = 0; i < nctx; ++i)
+        if (!ctxs[i]) return fail(QRM_INVALID_INPUT, "null context");
+    qrm_status s = check_uniform(ctxs[0], images, count, w, h, stride);
+    if (s != QRM_OK) return s;
+    if (count > 0 && !out) return fail(QRM_INVALID_INPUT, "null record buffer");
+    const int64_t t0 = now_ns();
+    std::vector<qrm_status> st(nctx, QRM_OK);
+    std::vector<std::string> err(nctx);
+    std::vector<qrm_host_stats> part(nctx);
+    auto run = [&](int i) {
+        const int64_t b = count * i / nctx, e = count * (i + 1) / nctx;
+        st[i] = qrm_detect_host(ctxs[i], images + b * stride, e - b, w, h, stride, first_draw + static_cast<uint64_t>(b),
+                                out + b, plan, mode, &part[i]);
+        if (st[i] != QRM_OK) err[i] = g_err;  // thread-local: carried to the caller below
+    };
+    std::vector<std::thread> th;
+    for (int i = 1; i < nctx; ++i) th.emplace_back(run, i);
+    run(0);
+    for (auto& t : th) t.join();
+    for (int i = 0; i < nctx; ++i)
+        if (st[i] != QRM_OK) return fail(st[i], "shard " + std::to_string(i) + ": " + err[i]);
+    if (stats) {
+        *stats = qrm_host_stats{};
+        for (const auto& p : part) {
+            stats->h2d_bytes += p.h2d_bytes;
+            stats->d2h_bytes += p.d2h_bytes;
+            stats->minibatches += p.minibatches;
+            stats->kernel_launches += p.kernel_launches;
+        }
+        stats->wall_ms = static_cast<double>(now_ns() - t0) / 1e6;
     }
     return QRM_OK;
 }

@@ -727,6 +727,7 @@ void write_ppm(const ImageBuffer& img, const std::filesystem::path& path) {
 
 struct GpuContext {
     qrm_ctx* h = nullptr;
+    std::vector<qrm_ctx*> shards;  // one per DetectionConfig::devices entry (multi-device batches)
 };
 
 static qrm_config gpu_config(const DetectionConfig& cfg) {
@@ -768,7 +769,10 @@ DetectionContext::DetectionContext(const DetectionConfig& cfg, int device)
     }
 }
 DetectionContext::~DetectionContext() {
-    if (gpu_) qrm_ctx_destroy(gpu_->h);
+    if (gpu_) {
+        for (qrm_ctx* s : gpu_->shards) qrm_ctx_destroy(s);
+        qrm_ctx_destroy(gpu_->h);
+    }
     delete gpu_;
 }
 
@@ -812,8 +816,25 @@ std::vector<DetectionRecord> DetectionContext::detect_many(std::span<const Image
                 pl.minibatch[k] = std::max(1, plan->minibatch[k]);
             }
         }
-        const qrm_status s = qrm_detect_host(gpu_->h, pinned, n, w, h, static_cast<int64_t>(bytes), first_draw,
-                                             rec.data(), &pl, 0, nullptr);  // mapped-window transfer
+        qrm_status s = QRM_OK;
+        if (cfg_.devices.size() > 1 && gpu_->shards.empty()) {
+            // one context per listed device, created on first use
+            qrm_config c = gpu_config(cfg_);
+            for (int dev : cfg_.devices) {
+                qrm_ctx* x = nullptr;
+                if ((s = qrm_ctx_create(dev, &c, &x)) != QRM_OK) break;
+                gpu_->shards.push_back(x);
+                if (cfg_.extractor == ExtractorKind::conv &&
+                    (s = qrm_ctx_set_extractor(x, QRM_EXTRACTOR_CONV, cfg_.conv_weight_seed)) != QRM_OK)
+                    break;
+            }
+        }
+        if (s == QRM_OK && gpu_->shards.size() > 1)
+            s = qrm_detect_host_multi(gpu_->shards.data(), static_cast<int>(gpu_->shards.size()), pinned, n, w, h,
+                                      static_cast<int64_t>(bytes), first_draw, rec.data(), &pl, 0, nullptr);
+        else if (s == QRM_OK)
+            s = qrm_detect_host(gpu_->h, pinned, n, w, h, static_cast<int64_t>(bytes), first_draw, rec.data(), &pl, 0,
+                                nullptr);  // mapped-window transfer
         cudaFreeHost(pinned);
         check(s);
     } else {

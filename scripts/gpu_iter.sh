@@ -1,3 +1,2 @@
 cd $GRAFT_REPO_ROOT
-timeout 900 python -m pytest tests -x -q -m gpu 2>&1 | tail -2
-timeout 600 python bench.py --steps 50 --no-cpu-baseline --rs-words 1000000 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['value'], d['ms_per_step'], d['roofline']['kernel_ms'], d['e2e']['value'])"
+timeout 600 python -m pytest tests/test_cpp_dropin.py -x -q -m gpu 2>&1 | tail -3

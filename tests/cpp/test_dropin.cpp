@@ -412,6 +412,11 @@ static void gpu_conv_detect() {
         if (d) CHECK(*r1[i].corrected == d->message && r1[i].errors_corrected == d->errors_corrected);
         CHECK(r1[i].bit_acc == bit_accuracy(r1[i].raw_bits, kcw));
     }
+    // sharded over several device contexts (here all on device 0): same records
+    DetectionConfig multi = cfg;
+    multi.devices = {0, 0, 0};
+    auto r4 = detect_batch(imgs, multi);
+    for (size_t i = 0; i < r4.size(); ++i) CHECK(semantic_equal(r1[i], r4[i]));
     // the spread-spectrum default is unaffected by a conv context alive beside it
     cfg.extractor = ExtractorKind::spread_spectrum;
     auto r3 = detect_batch(imgs, cfg);

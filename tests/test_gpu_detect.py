@@ -210,3 +210,25 @@ def test_bf16_tiles_match_reference_preprocess(qrm, cuda, ref):
                 x, y = ref.select_tile(256, 256, 64, strategy, 0, 9 + i)
                 want = cuda.tensor(pre[y:y + 64, x:x + 64]).to(cuda.bfloat16)
                 assert bool((t3[i].cpu() == want).all()), (strategy, h, w, i)
+
+
+@pytest.mark.gpu
+def test_detect_host_multi_equals_single(qrm, cuda):
+    """qrm_detect_host_multi shards a batch over contexts (one per GPU in
+    production; here several contexts on cuda:0 run concurrently from their own
+    host threads) and reproduces the single-context records exactly."""
+    cfg = qrm.DetectionConfig()
+    imgs = cuda.cat([qrm.make_corpus(cfg, 1000, 150), qrm.make_corpus(cfg, 5000, 101, embed=False)])
+    host = imgs.cpu().numpy()
+    with qrm.DetectionContext(cfg) as c0:
+        single, _ = c0.detect_host(host, 17)
+        ctxs = [qrm.DetectionContext(cfg) for _ in range(3)]
+        try:
+            for n in (1, 2, 3):
+                for mode in (0, 2):
+                    multi, st = qrm.detect_host_multi(ctxs[:n], host, 17, mode=mode)
+                    assert np.array_equal(multi, single), (n, mode)
+                    assert st["d2h_bytes"] == 24 * host.shape[0]
+        finally:
+            for c in ctxs:
+                c.close()
