@@ -267,11 +267,19 @@ def main():
     import paper_2509_02447_b200 as q
 
     world, rank, local = _dist()
+    # QRM_BENCH_SHARE_GPU=1 (test hook): ranks share the visible GPUs round-robin
+    # over gloo, to exercise the multi-rank code path on a one-GPU box.
+    share = os.environ.get("QRM_BENCH_SHARE_GPU") == "1"
+    if share:
+        local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
     cfg = q.DetectionConfig()
     ctx = q.DetectionContext(cfg, device=local)
@@ -302,7 +310,7 @@ def main():
     def max_over_ranks(x):
         if dist is None:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        t = torch.tensor([x], dtype=torch.float64, device="cpu" if share else dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
