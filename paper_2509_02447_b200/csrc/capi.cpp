@@ -246,7 +246,6 @@ DetectParams base_params(qrm_ctx* c, Workspace& w, int64_t count, qrm_record* ou
     p.tau_msg = c->tau_msg;
     p.tau_raw = c->tau_raw;
     p.fuse_t1 = (c->t == 1 && c->n - c->k <= 3) ? 1 : 0;
-    if (const char* e = getenv("QRM_EXP_FLAGS")) p.exp_flags = atoi(e);
     p.key_cw = c->key_cw;
     p.key_msg = c->key_msg;
     p.patterns = c->d_patterns;
@@ -1132,7 +1131,6 @@ qrm_status hidden_run(qrm_ctx* c, Workspace& W, const WindowSource& src, int64_t
             lp.act_out = lp.last ? nullptr : H.act[j & 1];
             lp.pool_out = lp.last ? H.pool : nullptr;
             lp.tiles = n;
-            if (const char* e = getenv("QRM_HIDDEN_DBG")) lp.dbg = atoi(e);  // timing experiments only
             QRM_LAUNCH(conv64_layer(H.tmap[(j - 1) & 1], H.tmap_st[j & 1], lp, c->sms, st));
         }
         HeadParams hp{};
@@ -1257,7 +1255,6 @@ QRM_EXPORT qrm_status qrm_hidden_debug_activation(qrm_ctx* c, const uint8_t* ima
         lp.act_out = lp.last ? nullptr : H.act[j & 1];
         lp.pool_out = lp.last ? H.pool : nullptr;
         lp.tiles = count;
-        if (const char* e = getenv("QRM_HIDDEN_DBG")) lp.dbg = atoi(e);
         QRM_LAUNCH(conv64_layer(H.tmap[(j - 1) & 1], H.tmap_st[j & 1], lp, c->sms, st));
     }
     if (stop_after == kHiddenLayers - 1)

@@ -164,12 +164,7 @@ __global__ void __launch_bounds__(kCorrThreads, 1) corr_detect_kernel(const __gr
         const int pitch = p.src.direct ? p.src.pitch : row_bytes;
         const uint32_t ring_u32 = smem_u32(ring);
         // K offset of this thread's 16 B, as (tile row, column) — stepped, no division per stage.
-        // Experiment (exp_flags bit 1): start each tile's K walk at a different
-        // chunk (integer sums are order-free) so the CTAs do not all read the same
-        // pattern lines from L2 at the same moment.
-        const int rot = (p.exp_flags & 2) ? static_cast<int>((blockIdx.x / S) * 7u % static_cast<unsigned>(kchunks)) : 0;
-        int krel = rot;
-        int kbyte = (kc_begin + rot) * kCorrKC + c * 16;
+        int kbyte = kc_begin * kCorrKC + c * 16;
         int trow = kbyte / row_bytes;
         int tcol = kbyte - trow * row_bytes;
         // (L2 prefetch of tile rows ahead of the ring — bulk or per line — was
@@ -196,13 +191,6 @@ __global__ void __launch_bounds__(kCorrThreads, 1) corr_detect_kernel(const __gr
             // Never block on the copies: the barrier phase completes when every
             // producer's copies for this stage have landed.
             cp_async_mbar_arrive(&sm.full[s]);
-            if (++krel == kchunks) {  // wrap to the start of this CTA's K range
-                krel = 0;
-                kbyte = kc_begin * kCorrKC + c * 16;
-                trow = kbyte / row_bytes;
-                tcol = kbyte - trow * row_bytes;
-                continue;
-            }
             kbyte += kCorrKC;
             tcol += kCorrKC;
             while (tcol >= row_bytes) {
@@ -256,7 +244,7 @@ __global__ void __launch_bounds__(kCorrThreads, 1) corr_detect_kernel(const __gr
                 if (p.dbg_stages && blockIdx.x < 8 && it < 128) p.dbg_stages[blockIdx.x * 256 + 128 + it] = clock64();
                 // The stage's bytes are in smem (written through the generic
                 // proxy by cp.async); order them before the async-proxy MMA reads.
-                if (!(p.exp_flags & 1)) fence_proxy_async_smem();
+                fence_proxy_async_smem();
                 tc_fence_after();
                 const uint32_t a_s = ring_u32 + s * kCorrStageBytes;
                 const uint64_t da = sw128_kmajor_desc(a_s);

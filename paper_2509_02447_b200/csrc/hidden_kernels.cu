@@ -196,7 +196,6 @@ __global__ void __launch_bounds__(kHThreads, 1)
         // issues. Descriptors are a per-block base plus compile-time offsets.
         const uint32_t idesc = idesc_bf16_f32(kHM, kHC);
         const uint64_t db0 = sw128_kmajor_desc(w_s);
-        const bool aligned_views = (p.dbg & 8) != 0;  // timing experiment only (wrong math)
         mbar_wait(&sm.w_full, 0);
         int i = 0;
         for (int64_t b = blockIdx.x; b < nblocks; b += gridDim.x, ++i) {
@@ -215,7 +214,7 @@ __global__ void __launch_bounds__(kHThreads, 1)
                     // A view: pixel row 64(1+dy)+dx of the 4-row buffer. It may start mid
                     // swizzle-atom; the base-offset field stays 0 (measured: the XOR
                     // pattern is taken from the absolute address bits TMA wrote with).
-                    const int view = aligned_views ? 64 * 128 : (64 * (1 + dy) + dx) * 128;
+                    const int view = (64 * (1 + dy) + dx) * 128;
                     // lanes whose horizontal neighbour is outside the image
                     const uint32_t m0 = dx < 0 ? 1u : 0u, m1 = dx > 0 ? 0x80000000u : 0u;
 #pragma unroll
@@ -243,8 +242,7 @@ __global__ void __launch_bounds__(kHThreads, 1)
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&sm.acc_empty[a]);
-            if (!(p.dbg & 16))  // timing experiment: skip the epilogue math/stores
-                conv_epilogue<1>(p, &tmap_out, acc, s_bias, sm.pool, o_s, q, h, lane, b / kHBlocks,
+            conv_epilogue<1>(p, &tmap_out, acc, s_bias, sm.pool, o_s, q, h, lane, b / kHBlocks,
                                  static_cast<int>(b % kHBlocks), i);
         }
         if (!p.last && h == 0 && lane == 0) bulk_wait<0>();
@@ -391,7 +389,6 @@ __global__ void __launch_bounds__(kHThreads, 1)
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive_cluster(empty0[a]);
-            if (!(p.dbg & 16))
             conv_epilogue<kPSlabs>(p, &tmap_out, acc, s_bias, sm.pool, o_s, q, h, lane, b / kPairBlocks,
                                    static_cast<int>(b % kPairBlocks) * 2 + static_cast<int>(rank), i);
         }

@@ -20,7 +20,6 @@ struct HiddenLayerParams {
     float* pool_out;                  // [T][32][64] per-block channel sums (last layer)
     int64_t tiles;
     int last;
-    int dbg;  // diagnostics: bit0 centre tap only, bit2 no lane masks
 };
 
 struct Conv0Params {

@@ -66,7 +66,6 @@ struct DetectParams {
     int32_t tau_msg, tau_raw;
     int32_t fuse_t1;    // epilogue may run the t=1 RS decoder itself
     int32_t tile_m;     // images per decode tile (<= 128 TMEM lanes); set by the launcher
-    int32_t exp_flags;  // experiment hooks (bit 0: skip the consumer proxy fence)
     unsigned long long* dbg_times;  // nullable: per-CTA phase timestamps (globaltimer ns), 8 per CTA
     long long* dbg_stages;          // nullable: CTAs 0-7, [cta][2][128] clock64 at producer issue / MMA full
     uint64_t key_cw, key_msg;
