@@ -159,6 +159,17 @@ QRM_EXPORT qrm_status qrm_hidden_detect_device(qrm_ctx* ctx, const uint8_t* imag
                                                int64_t image_stride, uint64_t first_draw, uint64_t weight_seed,
                                                float* logits, qrm_record* out, void* stream);
 
+/* qrm_detect_host with Algorithm 2 (resource-aware mini-batch scheduling,
+ * PAPER.md 6.2; lpt_schedule, sched.cpp:177-235) choosing the decode stream of
+ * every mini-batch: tasks are the plan's mini-batches, their latencies the
+ * decode time per image of this context's last qrm_warmup_profile(_mode)
+ * (uniform when none ran); LPT with balance slack lambda shards tasks into
+ * b_min-image pieces where needed. Records are identical to qrm_detect_host. */
+QRM_EXPORT qrm_status qrm_detect_host_lpt(qrm_ctx* ctx, const uint8_t* images, int64_t count, int w, int h,
+                                          int64_t image_stride, uint64_t first_draw, qrm_record* out,
+                                          const qrm_plan* plan, int mode, double lambda, int b_min,
+                                          qrm_host_stats* stats);
+
 /* qrm_detect_host over several contexts (normally one per device of the node,
  * SURVEY 8e): context i decodes the contiguous shard [count*i/n,
  * count*(i+1)/n) with its global draw indices on its own host thread, and its

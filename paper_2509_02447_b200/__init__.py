@@ -27,7 +27,7 @@ LIB_PATH = os.path.join(_HERE, "_lib", "libqrmark_b200.so")
 # Exported symbols of include/qrmark_gpu.h (checked by the CPU test suite).
 ABI_SYMBOLS = (
     "qrm_last_error", "qrm_abi_version", "qrm_device_count", "qrm_ctx_create", "qrm_ctx_destroy", "qrm_ctx_info",
-    "qrm_ctx_set_extractor", "qrm_ppm_read", "qrm_ppm_write", "qrm_ppm_read_batch", "qrm_records_json", "qrm_cache_hits", "qrm_attack_device", "qrm_warmup_profile_mode", "qrm_extract_tiles_device", "qrm_detect_host_multi",
+    "qrm_ctx_set_extractor", "qrm_ppm_read", "qrm_ppm_write", "qrm_ppm_read_batch", "qrm_records_json", "qrm_cache_hits", "qrm_attack_device", "qrm_warmup_profile_mode", "qrm_extract_tiles_device", "qrm_detect_host_multi", "qrm_detect_host_lpt",
     "qrm_detect_device", "qrm_detect_host", "qrm_detect_ragged", "qrm_extract_device", "qrm_preprocess_host",
     "qrm_rs_decode_packed_device", "qrm_rs_decode_symbols_device", "qrm_rs_stress_device", "qrm_rs_encode_packed",
     "qrm_verify_threshold", "qrm_make_corpus_device", "qrm_patterns_device", "qrm_allocate_streams",
@@ -98,6 +98,8 @@ def lib() -> C.CDLL:
         L.qrm_ctx_destroy.argtypes = [vp]
         L.qrm_ctx_info.argtypes = [vp, C.POINTER(u64), C.POINTER(u64), C.POINTER(i32), C.POINTER(i32)]
         L.qrm_ctx_set_extractor.argtypes = [vp, i32, u64]
+        L.qrm_detect_host_lpt.argtypes = [vp, vp, i64, i32, i32, i64, u64, vp, C.POINTER(_Plan), i32, C.c_double, i32,
+                                          C.POINTER(_HostStats)]
         L.qrm_detect_host_multi.argtypes = [C.POINTER(vp), i32, vp, i64, i32, i32, i64, u64, vp, C.POINTER(_Plan), i32,
                                             C.POINTER(_HostStats)]
         L.qrm_extract_tiles_device.argtypes = [vp, vp, i64, i32, i32, i64, u64, i32, vp, vp]
@@ -477,7 +479,7 @@ class DetectionContext:
         return s, raw
 
     def detect_host(self, images: np.ndarray | None = None, first_draw: int = 0, plan=None, mode: int = 0,
-                    out: np.ndarray | None = None, ptr: int | None = None, shape=None):
+                    out: np.ndarray | None = None, ptr: int | None = None, shape=None, lpt=None):
         """Host images (pinned or pageable) -> host records, through the stream executor.
 
         ``images``: numpy uint8 [B, H, W, 3] (or pass ``ptr``+``shape`` for a pinned torch buffer).
@@ -497,8 +499,13 @@ class DetectionContext:
         pl = None
         if plan is not None:
             pl = _Plan((C.c_int * 3)(*plan[0]), (C.c_int * 3)(*plan[1]))
-        _check(lib().qrm_detect_host(self._h, p, B, W, H, stride, first_draw, out.ctypes.data,
-                                     C.byref(pl) if pl is not None else None, mode, C.byref(st)))
+        if lpt is not None:  # (lambda, b_min): Algorithm 2 assigns the mini-batches to decode streams
+            _check(lib().qrm_detect_host_lpt(self._h, p, B, W, H, stride, first_draw, out.ctypes.data,
+                                             C.byref(pl) if pl is not None else None, mode, float(lpt[0]),
+                                             int(lpt[1]), C.byref(st)))
+        else:
+            _check(lib().qrm_detect_host(self._h, p, B, W, H, stride, first_draw, out.ctypes.data,
+                                         C.byref(pl) if pl is not None else None, mode, C.byref(st)))
         return out, {"wall_ms": st.wall_ms, "h2d_bytes": st.h2d_bytes, "d2h_bytes": st.d2h_bytes,
                      "minibatches": st.minibatches, "kernel_launches": st.kernel_launches}
 

@@ -190,6 +190,7 @@ struct qrm_ctx {
     std::vector<cudaStream_t> streams;
     qrm_plan plan{{1, 2, 1}, {4096, 4096, 4096}};
     std::unique_ptr<HostPool> pool;  // window staging workers (host pipeline, mode 2)
+    double decode_ms_per_image = 0.0;  // from the last warm-up profile (Algorithm 2 latencies)
     int extractor = QRM_EXTRACTOR_SPREAD_SPECTRUM;  // qrm_ctx_set_extractor
     uint64_t conv_seed = 7;
     // learned (conv) extractor: folded weights + activation ping-pong buffers
@@ -628,9 +629,21 @@ QRM_EXPORT qrm_status qrm_detect_ragged(qrm_ctx* c, const uint8_t* const* images
     return QRM_OK;
 }
 
-QRM_EXPORT qrm_status qrm_detect_host(qrm_ctx* c, const uint8_t* images, int64_t count, int w, int h,
-                                      int64_t stride, uint64_t first_draw, qrm_record* out, const qrm_plan* plan,
-                                      int mode, qrm_host_stats* stats) {
+}  // extern "C"
+
+namespace {
+
+// One unit of work of the host executor: images [first, first + count) decoded
+// on decode stream `stream` (its workspace slot). Round-robin mini-batches, or
+// the pieces of an Algorithm-2 schedule.
+struct HostPiece {
+    int64_t first, count;
+    int stream;
+};
+
+qrm_status detect_host_impl(qrm_ctx* c, const uint8_t* images, int64_t count, int w, int h, int64_t stride,
+                            uint64_t first_draw, qrm_record* out, const qrm_plan* plan, int mode,
+                            qrm_host_stats* stats, const std::vector<HostPiece>* pieces) {
     qrm_status s = check_uniform(c, images, count, w, h, stride);
     if (s != QRM_OK) return s;
     if (count > 0 && !out) return fail(QRM_INVALID_INPUT, "null record buffer");
@@ -712,20 +725,22 @@ QRM_EXPORT qrm_status qrm_detect_host(qrm_ctx* c, const uint8_t* images, int64_t
     }
 
     nstreams_used = nstreams;
-    ev.assign(4 * nstreams + 3 * nmb, nullptr);
+    const int64_t nwork = pieces ? static_cast<int64_t>(pieces->size()) : nmb;
+    ev.assign(4 * nstreams + 3 * nwork, nullptr);
     for (auto& e : ev) QRM_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     size_t evi = 0;
     std::vector<cudaEvent_t> slot_free(s1, nullptr);  // decode slot j reusable after its last finish
     double h2d = 0.0;
     int launches0 = static_cast<int>(g_launches.load());
-    for (int64_t b = 0; b < nmb; ++b) {
-        const int64_t first = b * mb;
-        const int64_t cnt = std::min(mb, count - first);
+    for (int64_t b = 0; b < nwork; ++b) {
+        const int64_t first = pieces ? (*pieces)[b].first : b * mb;
+        const int64_t cnt = pieces ? (*pieces)[b].count : std::min(mb, count - first);
+        const int lane = pieces ? (*pieces)[b].stream : static_cast<int>(b % s1);
         cudaStream_t xs = c->streams[b % s0];
         // the conv extractor's activation buffers are per context: one decode stream
-        cudaStream_t ds = c->streams[s0 + (c->extractor == QRM_EXTRACTOR_CONV ? 0 : b % s1)];
+        cudaStream_t ds = c->streams[s0 + (c->extractor == QRM_EXTRACTOR_CONV ? 0 : lane)];
         cudaStream_t cs = c->streams[s0 + s1 + b % s2];
-        const int slot = static_cast<int>(b % s1);
+        const int slot = lane;
         Workspace& W = c->ws[1 + slot];
         const uint8_t* src = dimg + first * stride;
         int64_t src_stride = stride;
@@ -845,6 +860,80 @@ QRM_EXPORT qrm_status qrm_detect_host(qrm_ctx* c, const uint8_t* images, int64_t
         stats->kernel_launches = static_cast<int>(g_launches.load()) - launches0;
     }
     return QRM_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+QRM_EXPORT qrm_status qrm_detect_host(qrm_ctx* c, const uint8_t* images, int64_t count, int w, int h,
+                                      int64_t stride, uint64_t first_draw, qrm_record* out, const qrm_plan* plan,
+                                      int mode, qrm_host_stats* stats) {
+    return detect_host_impl(c, images, count, w, h, stride, first_draw, out, plan, mode, stats, nullptr);
+}
+
+QRM_EXPORT qrm_status qrm_detect_host_lpt(qrm_ctx* c, const uint8_t* images, int64_t count, int w, int h,
+                                          int64_t stride, uint64_t first_draw, qrm_record* out, const qrm_plan* plan,
+                                          int mode, double lambda, int b_min, qrm_host_stats* stats) {
+    // Resource-aware mini-batch scheduling (section 6.2, Algorithm 2;
+    // lpt_schedule, sched.cpp:177-235) driving the executor: tasks are the
+    // mini-batches of plan.minibatch[1] images, their latency the decode stage's
+    // per-image time from this context's warm-up profile (uniform when none was
+    // taken) and their memory the staged-window bytes; LPT places them on the
+    // plan.streams[1] decode streams, sharding into b_min-image pieces where
+    // the balance slack lambda demands. Each piece runs on its assigned stream.
+    qrm_status s = check_uniform(c, images, count, w, h, stride);
+    if (s != QRM_OK) return s;
+    const qrm_plan P = plan ? *plan : c->plan;
+    if (P.streams[1] < 1 || P.minibatch[1] < 1) return fail(QRM_INVALID_INPUT, "plan has an empty stage");
+    if (b_min < 1) return fail(QRM_INVALID_INPUT, "b_min must be >= 1");
+    if (count == 0) return detect_host_impl(c, images, 0, w, h, stride, first_draw, out, plan, mode, stats, nullptr);
+    const int64_t mb = P.minibatch[1];
+    const int64_t nmb = (count + mb - 1) / mb;
+    if (nmb > INT32_MAX) return fail(QRM_INVALID_INPUT, "too many mini-batches");
+    const double per_image = c->decode_ms_per_image > 0.0 ? c->decode_ms_per_image : 1.0;
+    std::vector<sched::Task> tasks(static_cast<size_t>(nmb));
+    for (int64_t t = 0; t < nmb; ++t) {
+        const int64_t cnt = std::min(mb, count - t * mb);
+        tasks[t].id = static_cast<int>(t);
+        tasks[t].units = static_cast<int>(cnt);
+        tasks[t].latency = per_image * static_cast<double>(cnt);
+        tasks[t].memory = static_cast<double>(c->K) * static_cast<double>(cnt);
+    }
+    size_t free_b = 0, total_b = 0;
+    if ((s = set_device(c->device)) != QRM_OK) return s;
+    QRM_CUDA(cudaMemGetInfo(&free_b, &total_b));
+    sched::Schedule sch;
+    std::string err;
+    const int rc = sched::lpt_schedule(tasks, P.streams[1], lambda, static_cast<double>(free_b), b_min,
+                                       static_cast<int>(std::min<int64_t>(count, INT32_MAX)), sch, err);
+    if (rc) return fail(static_cast<qrm_status>(rc), err);
+    // pieces of a task are consecutive image ranges in placement order
+    std::vector<int64_t> offset(static_cast<size_t>(nmb), 0);
+    std::vector<HostPiece> pieces;
+    for (int st = 0; st < P.streams[1]; ++st)
+        for (const auto& t : sch.streams[st]) {
+            const int64_t first = static_cast<int64_t>(t.id) * mb + offset[t.id];
+            pieces.push_back(HostPiece{first, t.units, st});
+            offset[t.id] += t.units;
+        }
+    int64_t covered = 0;
+    for (int64_t t = 0; t < nmb; ++t) covered += offset[t];
+    if (covered != count) return fail(QRM_INFEASIBLE, "schedule does not cover the batch");
+    // issue in placement order, interleaving the streams (piece i of every stream, then i+1, ...)
+    std::vector<HostPiece> order;
+    std::vector<size_t> next(P.streams[1], 0);
+    std::vector<std::vector<HostPiece>> per(P.streams[1]);
+    for (const auto& pc : pieces) per[pc.stream].push_back(pc);
+    for (bool more = true; more;) {
+        more = false;
+        for (int st = 0; st < P.streams[1]; ++st)
+            if (next[st] < per[st].size()) {
+                order.push_back(per[st][next[st]++]);
+                more = true;
+            }
+    }
+    return detect_host_impl(c, images, count, w, h, stride, first_draw, out, plan, mode, stats, &order);
 }
 
 QRM_EXPORT qrm_status qrm_detect_host_multi(qrm_ctx* const* ctxs, int nctx, const uint8_t* images, int64_t count,
@@ -1625,6 +1714,7 @@ QRM_EXPORT qrm_status qrm_warmup_profile_mode(qrm_ctx* c, const uint8_t* images,
     time[0] = med(t0v);
     time[1] = med(t1v);
     time[2] = med(t2v);
+    c->decode_ms_per_image = time[1] / b0;
     memory[0] = static_cast<double>(mode == 0 ? c->K : img_bytes);
     memory[1] = static_cast<double>(c->K + sizeof(PendingEntry));
     memory[2] = static_cast<double>(sizeof(qrm_record));

@@ -232,3 +232,19 @@ def test_detect_host_multi_equals_single(qrm, cuda):
         finally:
             for c in ctxs:
                 c.close()
+
+
+@pytest.mark.gpu
+def test_algorithm2_schedule_drives_the_executor(qrm, cuda, cfg):
+    """qrm_detect_host_lpt: Algorithm 2 (lpt_schedule) places the mini-batches
+    (sharded into b_min pieces where the balance slack demands) on the decode
+    streams; the records equal the round-robin executor's for every setting."""
+    imgs = cuda.cat([qrm.make_corpus(cfg, 1000, 700), qrm.make_corpus(cfg, 5000, 300, embed=False)])
+    host = imgs.cpu().numpy()
+    with qrm.DetectionContext(cfg) as ctx:
+        want, _ = ctx.detect_host(host, 3, plan=([1, 3, 1], [128] * 3))
+        ctx.warmup_profile(host[:64], iters=2, b0=16, mode=0)  # latencies for the LPT tasks
+        for lam, bmin in ((1e9, 1), (0.0, 32), (0.1, 50), (0.5, 128)):
+            got, st = ctx.detect_host(host, 3, plan=([1, 3, 1], [128] * 3), lpt=(lam, bmin))
+            assert np.array_equal(got, want), (lam, bmin)
+            assert st["minibatches"] >= 8
