@@ -120,5 +120,7 @@ def test_conv_extractor_through_detect_entry_points(qrm, cuda):
         for mode in (0, 1, 2):
             out, st = ctx.detect_host(host, 5, plan=([1, 2, 1], [16, 16, 16]), mode=mode)
             assert np.array_equal(out, ref), mode
+        rag = ctx.detect_ragged(list(host), first_draw=5)  # staged-window path
+        assert np.array_equal(rag, ref)
     with pytest.raises(qrm.InvalidInput):
         qrm.DetectionContext(dataclasses.replace(base, extractor="cnn"))
