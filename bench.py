@@ -371,7 +371,8 @@ def main():
         return st
 
     e2e = {}
-    for mode in (2, 0, 1):
+    ctx.set_transfer_split(0.7)  # mode 3: 70 % zero-copy, 30 % host-staged (scripts/host_modes_native.cpp sweep)
+    for mode in (2, 3, 0, 1):
         for i in range(args.warmup):
             e2e_step(i, mode)
         barrier()
@@ -519,6 +520,7 @@ def main():
                              "draw range, 4 x 50 MB of tile windows per rotation > 126 MB L2)",
                        "e2e_modes": {"mapped_window_zero_copy (mode 0, headline)": e2e[0],
                                      "staged_window_host_gather (mode 2)": e2e[2],
+                                     "zero_copy_70_plus_staged_30 (mode 3)": e2e[3],
                                      "full_image_h2d (mode 1)": e2e[1]},
                        "e2e_plan": {"streams": plan[0], "minibatch": plan[1]}},
             "e2e": e2e[0],

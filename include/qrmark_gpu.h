@@ -130,8 +130,11 @@ QRM_EXPORT qrm_status qrm_detect_device(qrm_ctx* ctx, const uint8_t* images, int
  * mode 0: window-only transfer (the tile window is read from mapped pinned host
  * memory by the decode kernel); mode 1: full-image H2D copies; mode 2: staged
  * window transfer (a host worker pool copies each image's l x l window into
- * pinned staging, one contiguous H2D per mini-batch). Host images are
- * registered (page-locked) for the call if they are not pinned already. */
+ * pinned staging, one contiguous H2D per mini-batch); mode 3: both at once on
+ * each mini-batch -- a share (qrm_ctx_set_transfer_split, default 0.5) of the
+ * windows fetched zero-copy while the workers stage the rest for the copy
+ * engine. Host images are registered (page-locked) for the call if they are
+ * not pinned already. */
 QRM_EXPORT qrm_status qrm_detect_host(qrm_ctx* ctx, const uint8_t* images, int64_t count, int w, int h,
                                       int64_t image_stride, uint64_t first_draw, qrm_record* out,
                                       const qrm_plan* plan, int mode, qrm_host_stats* stats);
@@ -200,6 +203,11 @@ QRM_EXPORT qrm_status qrm_extract_tiles_device(qrm_ctx* ctx, const uint8_t* imag
 #define QRM_EXTRACTOR_SPREAD_SPECTRUM 0
 #define QRM_EXTRACTOR_CONV 1
 QRM_EXPORT qrm_status qrm_ctx_set_extractor(qrm_ctx* ctx, int kind, uint64_t weight_seed);
+
+/* Host pipeline mode 3: the share of each mini-batch's windows the transfer
+ * kernel fetches zero-copy; the rest go through pinned staging and the copy
+ * engine. Both paths give the same records. */
+QRM_EXPORT qrm_status qrm_ctx_set_transfer_split(qrm_ctx* ctx, double zero_copy_fraction);
 
 /* ---- robustness attacks -------------------------------- */
 

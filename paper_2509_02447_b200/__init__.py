@@ -27,7 +27,7 @@ LIB_PATH = os.path.join(_HERE, "_lib", "libqrmark_b200.so")
 # Exported symbols of include/qrmark_gpu.h (checked by the CPU test suite).
 ABI_SYMBOLS = (
     "qrm_last_error", "qrm_abi_version", "qrm_device_count", "qrm_ctx_create", "qrm_ctx_destroy", "qrm_ctx_info",
-    "qrm_ctx_set_extractor", "qrm_ppm_read", "qrm_ppm_write", "qrm_ppm_read_batch", "qrm_records_json", "qrm_cache_hits", "qrm_attack_device", "qrm_warmup_profile_mode", "qrm_extract_tiles_device", "qrm_detect_host_multi", "qrm_detect_host_lpt",
+    "qrm_ctx_set_extractor", "qrm_ppm_read", "qrm_ppm_write", "qrm_ppm_read_batch", "qrm_records_json", "qrm_cache_hits", "qrm_attack_device", "qrm_warmup_profile_mode", "qrm_extract_tiles_device", "qrm_detect_host_multi", "qrm_detect_host_lpt", "qrm_ctx_set_transfer_split",
     "qrm_detect_device", "qrm_detect_host", "qrm_detect_ragged", "qrm_extract_device", "qrm_preprocess_host",
     "qrm_rs_decode_packed_device", "qrm_rs_decode_symbols_device", "qrm_rs_stress_device", "qrm_rs_encode_packed",
     "qrm_verify_threshold", "qrm_make_corpus_device", "qrm_patterns_device", "qrm_allocate_streams",
@@ -98,6 +98,7 @@ def lib() -> C.CDLL:
         L.qrm_ctx_destroy.argtypes = [vp]
         L.qrm_ctx_info.argtypes = [vp, C.POINTER(u64), C.POINTER(u64), C.POINTER(i32), C.POINTER(i32)]
         L.qrm_ctx_set_extractor.argtypes = [vp, i32, u64]
+        L.qrm_ctx_set_transfer_split.argtypes = [vp, C.c_double]
         L.qrm_detect_host_lpt.argtypes = [vp, vp, i64, i32, i32, i64, u64, vp, C.POINTER(_Plan), i32, C.c_double, i32,
                                           C.POINTER(_HostStats)]
         L.qrm_detect_host_multi.argtypes = [C.POINTER(vp), i32, vp, i64, i32, i32, i64, u64, vp, C.POINTER(_Plan), i32,
@@ -483,6 +484,8 @@ class DetectionContext:
         """Host images (pinned or pageable) -> host records, through the stream executor.
 
         ``images``: numpy uint8 [B, H, W, 3] (or pass ``ptr``+``shape`` for a pinned torch buffer).
+        ``mode``: transfer stage -- 0 zero-copy window fetch, 1 full-image H2D, 2 host-staged
+        windows, 3 both 0 and 2 on each mini-batch (see set_transfer_split).
         Returns (records structured array, stats dict)."""
         if images is not None:
             images = np.ascontiguousarray(images, dtype=np.uint8)
@@ -519,6 +522,10 @@ class DetectionContext:
         out = np.zeros(n, dtype=RECORD_DTYPE)
         _check(lib().qrm_detect_ragged(self._h, ptrs, ws, hs, n, first_draw, out.ctypes.data))
         return out
+
+    def set_transfer_split(self, zero_copy_fraction: float):
+        """Host pipeline mode 3: share of each mini-batch's windows fetched zero-copy."""
+        _check(lib().qrm_ctx_set_transfer_split(self._h, float(zero_copy_fraction)))
 
     def set_plan(self, streams, minibatch):
         pl = _Plan((C.c_int * 3)(*streams), (C.c_int * 3)(*minibatch))

@@ -13,6 +13,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <immintrin.h>
 #include <atomic>
 #include <chrono>
 #include <cmath>
@@ -189,7 +190,10 @@ struct qrm_ctx {
     std::vector<Workspace> ws;  // [0]: device API; [1..]: host pipeline slots
     std::vector<cudaStream_t> streams;
     qrm_plan plan{{1, 2, 1}, {4096, 4096, 4096}};
-    std::unique_ptr<HostPool> pool;  // window staging workers (host pipeline, mode 2)
+    std::unique_ptr<HostPool> pool;  // window staging workers (host pipeline, modes 2 and 3)
+    cudaStream_t copy_stream = nullptr;  // mode 3: copy-engine H2D of the staged windows
+    double hybrid_fraction = 0.5;        // mode 3: share of each mini-batch fetched zero-copy
+    int64_t stage_piece = 512;           // modes 2/3: windows gathered per H2D
     double decode_ms_per_image = 0.0;  // from the last warm-up profile (Algorithm 2 latencies)
     int extractor = QRM_EXTRACTOR_SPREAD_SPECTRUM;  // qrm_ctx_set_extractor
     uint64_t conv_seed = 7;
@@ -504,6 +508,7 @@ QRM_EXPORT void qrm_ctx_destroy(qrm_ctx* c) {
     cudaSetDevice(c->device);
     for (auto& w : c->ws) w.release();
     for (auto s : c->streams) cudaStreamDestroy(s);
+    if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
     cudaFree(c->d_patterns);
     cudaFree(c->d_colsum);
     cudaFree(c->d_records);
@@ -647,8 +652,9 @@ qrm_status detect_host_impl(qrm_ctx* c, const uint8_t* images, int64_t count, in
     qrm_status s = check_uniform(c, images, count, w, h, stride);
     if (s != QRM_OK) return s;
     if (count > 0 && !out) return fail(QRM_INVALID_INPUT, "null record buffer");
-    if (mode < 0 || mode > 2)
-        return fail(QRM_INVALID_INPUT, "mode must be 0 (mapped window), 1 (full image) or 2 (staged window)");
+    if (mode < 0 || mode > 3)
+        return fail(QRM_INVALID_INPUT,
+                    "mode must be 0 (mapped window), 1 (full image), 2 (staged window) or 3 (mapped + staged)");
     if ((s = set_device(c->device)) != QRM_OK) return s;
     const qrm_plan P = plan ? *plan : c->plan;
     for (int k = 0; k < 3; ++k)
@@ -702,11 +708,13 @@ qrm_status detect_host_impl(qrm_ctx* c, const uint8_t* images, int64_t count, in
     const int64_t img_bytes = static_cast<int64_t>(w) * h * 3;
     int up, sw, sh, xo, yo;
     geometry(w, h, up, sw, sh, xo, yo);
-    if (mode == 2 && up) mode = 1;  // upscaled inputs need the device bilinear gather
+    if ((mode == 2 || mode == 3) && up) mode = 1;  // upscaled inputs need the device bilinear gather
+    if (mode == 3 && !(direct_ok(c, dimg, w, h, stride) && (3 * c->l) % 16 == 0)) mode = 2;
     if (mode == 1)
         for (int j = 0; j < s1; ++j)
             if ((s = ensure(c->ws[1 + j].images, c->ws[1 + j].images_cap, mb * img_bytes)) != QRM_OK) return s;
-    if (mode == 2) {
+    if (mode == 2 || mode == 3) {
+        if (mode == 3 && !c->copy_stream) QRM_CUDA(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
         if (!c->pool) {
             const unsigned hc = std::thread::hardware_concurrency();
             c->pool = std::make_unique<HostPool>(static_cast<int>(std::max(1u, std::min(hc ? hc - 1 : 1u, 31u))));
@@ -726,7 +734,7 @@ qrm_status detect_host_impl(qrm_ctx* c, const uint8_t* images, int64_t count, in
 
     nstreams_used = nstreams;
     const int64_t nwork = pieces ? static_cast<int64_t>(pieces->size()) : nmb;
-    ev.assign(4 * nstreams + 3 * nwork, nullptr);
+    ev.assign(4 * nstreams + 4 * nwork, nullptr);
     for (auto& e : ev) QRM_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     size_t evi = 0;
     std::vector<cudaEvent_t> slot_free(s1, nullptr);  // decode slot j reusable after its last finish
@@ -745,42 +753,81 @@ qrm_status detect_host_impl(qrm_ctx* c, const uint8_t* images, int64_t count, in
         const uint8_t* src = dimg + first * stride;
         int64_t src_stride = stride;
         if (slot_free[slot]) QRM_CUDA(cudaStreamWaitEvent(xs, slot_free[slot], 0));
-        if (mode == 2) {
-            // stage 0 (CPU part): copy each image's l x l window into pinned
-            // staging with the worker pool, then one contiguous H2D.
-            if (slot_free[slot]) QRM_CUDA(cudaEventSynchronize(slot_free[slot]));
-            uint8_t* hs = W.host_stage;
-            const int l = c->l, rowb = 3 * l, pitch = 3 * w;
+        if (mode == 2 || mode == 3) {
+            // stage 0. Mode 3: the transfer kernel pulls the first `nz` windows
+            // over PCIe (zero-copy) while the CPU workers copy the others into
+            // pinned staging for one copy-engine H2D on the copy stream; the two
+            // share the link (scripts/pcie_probe.cu: 47.8 GB/s zero-copy alone,
+            // 50.9 GB/s half and half). Mode 2: all windows through staging.
             const int K = c->K;
+            const int64_t nz = mode == 3 ? std::min(cnt, static_cast<int64_t>(c->hybrid_fraction * cnt)) : 0;
+            if ((s = ensure(W.stage, W.stage_cap, mb * K)) != QRM_OK) return s;
+            WindowSource hs{};
+            hs.base = src;
+            hs.image_stride = stride;
+            hs.pitch = w * 3;
+            hs.x_off = xo;
+            hs.y_off = yo;
+            hs.direct = 1;
+            hs.l = c->l;
+            hs.strategy = c->cfg.tile_strategy;
+            hs.tile_seed = c->cfg.tile_seed;
+            hs.first_draw = first_draw + static_cast<uint64_t>(first);
+            if (nz > 0) QRM_LAUNCH(launch_fetch_windows(hs, nz, K, W.stage, c->sms, xs));
+            if (slot_free[slot]) QRM_CUDA(cudaEventSynchronize(slot_free[slot]));  // host_stage reusable
+            uint8_t* hst = W.host_stage;
+            const int l = c->l, rowb = 3 * l, pitch = 3 * w;
             const auto& cfg = c->cfg;
-            c->pool->parallel_for(cnt, 64, [&](int64_t i0, int64_t i1) {
-                for (int64_t i = i0; i < i1; ++i) {
-                    int tx, ty;
-                    select_tile(kWorkingSize, kWorkingSize, l, cfg.tile_strategy, cfg.tile_seed,
-                                first_draw + static_cast<uint64_t>(first + i), tx, ty);
-                    const uint8_t* src0 = images + (first + i) * stride + static_cast<int64_t>(yo + ty) * pitch +
-                                          static_cast<int64_t>(xo + tx) * 3;
-                    uint8_t* dst = hs + i * K;
-                    if (rowb == 192)  // l = 64: fixed-size rows compile to vector moves
-                        for (int r = 0; r < 64; ++r) std::memcpy(dst + r * 192, src0 + static_cast<int64_t>(r) * pitch, 192);
-                    else
-                        for (int r = 0; r < l; ++r) std::memcpy(dst + r * rowb, src0 + static_cast<int64_t>(r) * pitch, rowb);
-                }
-            });
-            QRM_CUDA(cudaMemcpyAsync(W.stage, hs, cnt * K, cudaMemcpyHostToDevice, xs));
+            cudaStream_t cps = mode == 3 ? c->copy_stream : xs;
+            if (mode == 3 && slot_free[slot]) QRM_CUDA(cudaStreamWaitEvent(cps, slot_free[slot], 0));
+            // the staged windows in pieces: the copy engine moves piece j while
+            // the workers gather piece j + 1
+            const int64_t piece = c->stage_piece;
+            for (int64_t p0 = 0; p0 < cnt - nz; p0 += piece) {
+                const int64_t p1 = std::min(cnt - nz, p0 + piece);
+                c->pool->parallel_for(p1 - p0, 32, [&](int64_t j0, int64_t j1) {
+                    for (int64_t i = p0 + j0; i < p0 + j1; ++i) {
+                        const int64_t img = first + nz + i;
+                        int tx, ty;
+                        select_tile(kWorkingSize, kWorkingSize, l, cfg.tile_strategy, cfg.tile_seed,
+                                    first_draw + static_cast<uint64_t>(img), tx, ty);
+                        const uint8_t* src0 = images + img * stride + static_cast<int64_t>(yo + ty) * pitch +
+                                              static_cast<int64_t>(xo + tx) * 3;
+                        uint8_t* dst = hst + i * K;
+                        if (rowb == 192) {
+                            // l = 64: non-temporal 16-B stores. Staging written through
+                            // the cache stays dirty in the workers' L2s and the copy
+                            // engine's reads of it crawl (50 MB: 3.0 ms vs 0.92 ms)
+                            for (int r = 0; r < 64; ++r) {
+                                const __m128i* s16 = reinterpret_cast<const __m128i*>(src0 + static_cast<int64_t>(r) * pitch);
+                                __m128i* d16 = reinterpret_cast<__m128i*>(dst + r * 192);
+                                for (int k = 0; k < 12; ++k) _mm_stream_si128(d16 + k, _mm_loadu_si128(s16 + k));
+                            }
+                        } else
+                            for (int r = 0; r < l; ++r)
+                                std::memcpy(dst + r * rowb, src0 + static_cast<int64_t>(r) * pitch, rowb);
+                    }
+                    _mm_sfence();  // the streaming stores are globally visible before the H2D is issued
+                });
+                QRM_CUDA(cudaMemcpyAsync(W.stage + (nz + p0) * K, hst + p0 * K, (p1 - p0) * K, cudaMemcpyHostToDevice,
+                                         cps));
+            }
             h2d += static_cast<double>(K) * cnt;
             cudaEvent_t e_in = ev[evi++];
             QRM_CUDA(cudaEventRecord(e_in, xs));
             QRM_CUDA(cudaStreamWaitEvent(ds, e_in, 0));
-            WindowSource ws{};
+            if (mode == 3) {
+                cudaEvent_t e_cp = ev[evi++];
+                QRM_CUDA(cudaEventRecord(e_cp, cps));
+                QRM_CUDA(cudaStreamWaitEvent(ds, e_cp, 0));
+            }
+            WindowSource ws = hs;
             ws.base = W.stage;
             ws.image_stride = K;
             ws.pitch = rowb;
             ws.direct = 0;
-            ws.l = l;
-            ws.strategy = cfg.tile_strategy;
-            ws.tile_seed = cfg.tile_seed;
-            ws.first_draw = first_draw + static_cast<uint64_t>(first);
+            ws.x_off = 0;
+            ws.y_off = 0;
             cudaEvent_t e_mid = ev[evi++];
             if ((s = run_detect(c, W, ws, cnt, c->d_records + first, nullptr, nullptr, ds, e_mid, cs)) != QRM_OK)
                 return s;
@@ -852,6 +899,7 @@ qrm_status detect_host_impl(qrm_ctx* c, const uint8_t* images, int64_t count, in
         slot_free[slot] = e_done;
     }
     for (int i = 0; i < nstreams; ++i) QRM_CUDA(cudaStreamSynchronize(c->streams[i]));
+    if (c->copy_stream) QRM_CUDA(cudaStreamSynchronize(c->copy_stream));
     if (stats) {
         stats->wall_ms = static_cast<double>(now_ns() - t0) / 1e6;
         stats->h2d_bytes = h2d;
@@ -1306,6 +1354,14 @@ QRM_EXPORT qrm_status qrm_extract_tiles_device(qrm_ctx* c, const uint8_t* images
     if (r != CUDA_SUCCESS) return fail(QRM_CUDA_ERROR, "cuTensorMapEncodeTiled (tiles) failed (" + std::to_string(r) + ")");
     TileBf16Params p{src, count, c->K, channels, static_cast<uint16_t*>(out)};
     QRM_LAUNCH(launch_tile_bf16(map, p, c->sms, st));
+    return QRM_OK;
+}
+
+QRM_EXPORT qrm_status qrm_ctx_set_transfer_split(qrm_ctx* c, double zero_copy_fraction) {
+    if (!c) return fail(QRM_INVALID_INPUT, "null context");
+    if (!(zero_copy_fraction >= 0.0 && zero_copy_fraction <= 1.0))
+        return fail(QRM_INVALID_INPUT, "zero-copy fraction must be in [0, 1]");
+    c->hybrid_fraction = zero_copy_fraction;
     return QRM_OK;
 }
 

@@ -10,7 +10,11 @@ host = torch.empty(pool.shape, dtype=torch.uint8, pin_memory=True); host.copy_(p
 recs_pinned = torch.empty((B, q.RECORD_DTYPE.itemsize), dtype=torch.uint8, pin_memory=True)
 recs = recs_pinned.numpy().view(q.RECORD_DTYPE).reshape(-1)
 with q.DetectionContext(cfg) as ctx:
-    for mode in (0, 2, 1):
+    modes = [int(m) for m in os.environ.get("E2E_MODES", "0,2,1").split(",")]
+    fracs = [float(f) for f in os.environ.get("E2E_FRACS", "0.5").split(",")]
+    for mode, frac in [(m, f) for m in modes for f in (fracs if m == 3 else [None])]:
+        if frac is not None:
+            ctx.set_transfer_split(frac)
         for streams, mb in (([1, 2, 1], 2048), ([1, 2, 1], 1024), ([2, 2, 2], 1024), ([1, 1, 1], 4096)):
             plan = (streams, [mb] * 3)
             def step(i):
@@ -22,4 +26,4 @@ with q.DetectionContext(cfg) as ctx:
             for i in range(n): step(3 + i)
             dt = time.perf_counter() - t0
             assert recs["verified"].all()
-            print(json.dumps({"mode": mode, "streams": streams, "mb": mb, "img_per_s": round(B * n / dt)}), flush=True)
+            print(json.dumps({"mode": mode, "frac": frac, "streams": streams, "mb": mb, "img_per_s": round(B * n / dt)}), flush=True)

@@ -178,15 +178,22 @@ def test_preprocess_matches_reference(qrm, ref):
         assert np.array_equal(qrm.preprocess(img), ref.preprocess(img))
 
 
-@pytest.mark.parametrize("mode", [0, 1])
+@pytest.mark.parametrize("mode", [0, 1, 2, 3])
 def test_host_pipeline_equals_device(qrm, cuda, cfg, mode):
     imgs = qrm.make_corpus(cfg, 12000, 1000)
     host = imgs.cpu().numpy()
     with qrm.DetectionContext(cfg) as ctx:
         dev = qrm.records_from_device(ctx.detect_device(imgs, first_draw=50))
-        rec, st = ctx.detect_host(host, first_draw=50, plan=([2, 3, 2], [128, 128, 128]), mode=mode)
-    assert np.array_equal(rec.view(np.uint8), dev.view(np.uint8))
-    assert st["minibatches"] == 8
+        # mode 3: the zero-copy / staged split at the edges and in between
+        for frac in ((0.0, 0.37, 0.5, 1.0) if mode == 3 else (None,)):
+            if frac is not None:
+                ctx.set_transfer_split(frac)
+            rec, st = ctx.detect_host(host, first_draw=50, plan=([2, 3, 2], [128, 128, 128]), mode=mode)
+            assert np.array_equal(rec.view(np.uint8), dev.view(np.uint8)), frac
+            assert st["minibatches"] == 8
+        if mode == 3:
+            with pytest.raises(qrm.QrmError):
+                ctx.set_transfer_split(1.5)
 
 
 @pytest.mark.gpu
