@@ -424,6 +424,9 @@ __global__ void __launch_bounds__(kC0Threads) conv0_kernel(const __grid_constant
     __shared__ float lut[256];
     __shared__ float bsh[kHC];
     __shared__ __align__(16) uint8_t rows[4][3 * kHSide];
+    // the block's 4 input rows normalised, channel-planar, x + 1 (columns -1 and
+    // 64 stay 0: the zero padding), so each im2col tap is one conflict-free LDS
+    __shared__ float rowf[4][3][kHSide + 4];
     __shared__ uint64_t done;
     __shared__ uint32_t tmem_slot;
 
@@ -442,6 +445,7 @@ __global__ void __launch_bounds__(kC0Threads) conv0_kernel(const __grid_constant
         lut[v] = __uint_as_float(t);
     }
     if (tid < kHC) bsh[tid] = p.b0[tid];
+    for (int i = tid; i < 4 * 3 * (kHSide + 4); i += kC0Threads) (&rowf[0][0][0])[i] = 0.0f;
     {
         const uint4* src = reinterpret_cast<const uint4*>(p.w0);
         uint4* dst = reinterpret_cast<uint4*>(b_tile);
@@ -480,21 +484,26 @@ __global__ void __launch_bounds__(kC0Threads) conv0_kernel(const __grid_constant
         if (have) reinterpret_cast<uint4*>(rows[tid / kRow16])[tid % kRow16] = pre;
         __syncthreads();
         have = fetch(b + gridDim.x, pre);
+        // normalise each input byte once (768 table lookups per block instead of
+        // 27 per pixel); zero padding is in the normalised domain: rows outside
+        // the tile contribute 0.0, not lut[0] = -1
+#pragma unroll
+        for (int j = 0; j < 4 * 3 * kHSide / kC0Threads; ++j) {
+            const int i = tid + j * kC0Threads;
+            const int r = i / (3 * kHSide), byte = i - r * (3 * kHSide);
+            const int sy = y0 - 1 + r;
+            rowf[r][byte % 3][byte / 3 + 1] = (sy >= 0 && sy < kHSide) ? lut[rows[r][byte]] : 0.0f;
+        }
+        __syncthreads();
 
         // im2col row of pixel (y0 + tid/64, tid%64): k = tap*3 + c, tap = 3(dy+1) + (dx+1)
         {
             const int ry = 1 + (tid >> 6), px = tid & 63;
             float x[kC0K];
 #pragma unroll
-            for (int t = 0; t < 9; ++t) {
-                // zero padding is in the normalised domain: taps outside the tile
-                // (either axis) contribute 0.0, not lut[0] = -1
-                const int sx = px + t % 3 - 1, sy = y0 + ry + t / 3 - 2;
-                const bool in = sx >= 0 && sx < kHSide && sy >= 0 && sy < kHSide;
-                const uint8_t* rp = rows[ry + t / 3 - 1];
+            for (int t = 0; t < 9; ++t)
 #pragma unroll
-                for (int c = 0; c < 3; ++c) x[t * 3 + c] = in ? lut[rp[sx * 3 + c]] : 0.0f;
-            }
+                for (int c = 0; c < 3; ++c) x[t * 3 + c] = rowf[ry + t / 3 - 1][c][px + t % 3];
 #pragma unroll
             for (int k = 27; k < kC0K; ++k) x[k] = 0.0f;
             const uint32_t row = smem_u32(a_tile) + tid * 128;
