@@ -192,6 +192,7 @@ struct qrm_ctx {
     qrm_plan plan{{1, 2, 1}, {4096, 4096, 4096}};
     std::unique_ptr<HostPool> pool;  // window staging workers (host pipeline, modes 2 and 3)
     cudaStream_t copy_stream = nullptr;  // mode 3: copy-engine H2D of the staged windows
+    std::vector<cudaEvent_t> events;     // host pipeline events, reused call to call
     double hybrid_fraction = 0.5;        // mode 3: share of each mini-batch fetched zero-copy
     int64_t stage_piece = 512;           // modes 2/3: windows gathered per H2D
     double decode_ms_per_image = 0.0;  // from the last warm-up profile (Algorithm 2 latencies)
@@ -509,6 +510,7 @@ QRM_EXPORT void qrm_ctx_destroy(qrm_ctx* c) {
     for (auto& w : c->ws) w.release();
     for (auto s : c->streams) cudaStreamDestroy(s);
     if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
+    for (auto e : c->events) cudaEventDestroy(e);
     cudaFree(c->d_patterns);
     cudaFree(c->d_colsum);
     cudaFree(c->d_records);
@@ -665,14 +667,12 @@ qrm_status detect_host_impl(qrm_ctx* c, const uint8_t* images, int64_t count, in
     // Host buffers must be page-locked and mapped; register them for the call if not.
     const int64_t in_bytes = (count - 1) * stride + static_cast<int64_t>(w) * h * 3;
     bool reg_in = false, reg_out = false;
-    std::vector<cudaEvent_t> ev;
     int nstreams_used = 0;
     // Every exit path (errors included) drains the streams this call used
-    // before it releases the events and unregisters the caller's buffers.
+    // before the context's events are reused and the caller's buffers unregistered.
     auto cleanup = on_exit([&] {
         for (int i = 0; i < nstreams_used; ++i) cudaStreamSynchronize(c->streams[i]);
-        for (auto e : ev)
-            if (e) cudaEventDestroy(e);
+        if (c->copy_stream) cudaStreamSynchronize(c->copy_stream);
         if (reg_in) cudaHostUnregister(const_cast<uint8_t*>(images));
         if (reg_out) cudaHostUnregister(out);
     });
@@ -734,8 +734,14 @@ qrm_status detect_host_impl(qrm_ctx* c, const uint8_t* images, int64_t count, in
 
     nstreams_used = nstreams;
     const int64_t nwork = pieces ? static_cast<int64_t>(pieces->size()) : nmb;
-    ev.assign(4 * nstreams + 4 * nwork, nullptr);
-    for (auto& e : ev) QRM_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    // events come from the context's pool (creating ~20 per call cost ~50 us)
+    const size_t nev = static_cast<size_t>(4 * nstreams + 4 * nwork);
+    while (c->events.size() < nev) {
+        cudaEvent_t e;
+        QRM_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        c->events.push_back(e);
+    }
+    const std::vector<cudaEvent_t>& ev = c->events;
     size_t evi = 0;
     std::vector<cudaEvent_t> slot_free(s1, nullptr);  // decode slot j reusable after its last finish
     double h2d = 0.0;
