@@ -342,7 +342,8 @@ qrm_status run_detect(qrm_ctx* c, Workspace& w, const WindowSource& src, int64_t
         QRM_CUDA(cudaStreamWaitEvent(finish_stream, mid_event, 0));
         fs = finish_stream;
     }
-    QRM_LAUNCH(launch_detect_finish(p, std::max(1, c->t), c->sms, fs));
+    // t = 1 codes leave nothing pending (the decode kernel resolves its own ties)
+    if (!p.fuse_t1) QRM_LAUNCH(launch_detect_finish(p, std::max(1, c->t), c->sms, fs));
     return QRM_OK;
 }
 
@@ -1296,7 +1297,7 @@ qrm_status hidden_run(qrm_ctx* c, Workspace& W, const WindowSource& src, int64_t
         QRM_LAUNCH(launch_hidden_head(hp, st));
         DetectParams fp = base_params(c, W, n, out + off, nullptr, nullptr);
         fp.src = cs;
-        QRM_LAUNCH(launch_detect_finish(fp, std::max(1, c->t), c->sms, st));  // general-t codes only
+        if (!fp.fuse_t1) QRM_LAUNCH(launch_detect_finish(fp, std::max(1, c->t), c->sms, st));  // general-t codes
     }
     return QRM_OK;
 }

@@ -11,8 +11,9 @@
 // sum_px float(v/127.5-1) P is the sign of the EXACT integer
 //   S = sum_px (2v - 255) P = 2 D - 255 colsum(P)
 // except when S == 0, where the reference's double rounding decides; those
-// (image, bit) pairs are re-evaluated with the reference's exact sequential
-// double summation by detect_finish_kernel, so hard bits are bit-exact.
+// (image, bit) pairs are re-evaluated exactly (tie_bit_exact below; for codes
+// the epilogue cannot finish, by detect_finish_kernel), so hard bits are
+// bit-exact.
 //
 // corr_detect_kernel: one CTA = 128 images (UMMA M) x 64 bit columns (N) x a
 // K range. Warps 0-3 stream 128-byte K chunks of the 128 tile windows
@@ -54,6 +55,13 @@ struct CorrSmem {
     RsSmem rs;
     // Split-K partials from the cluster: [rank][row within my 128/S rows][kRedStride]
     alignas(16) int32_t red[kCorrM * kRedStride];
+    // t = 1 codes: this CTA's images with tied bits, finished after the epilogue
+    struct TieEntry {
+        int64_t image;
+        uint64_t tie_mask, raw;
+    } ties[kCorrM];
+    int nties;
+    long long tie_lut[256];  // float(v/127.5 - 1) * 2^31, exact integers
 };
 
 constexpr size_t kCorrSmemBytes = 1024 /*align slack*/ + kCorrStages * kCorrStageBytes + sizeof(CorrSmem);
@@ -62,7 +70,7 @@ constexpr size_t kCorrSmemBytes = 1024 /*align slack*/ + kCorrStages * kCorrStag
 // S_i > 0 (harden), tie i = S_i == 0; pack MSB-first; t = 1 code without ties:
 // RS-correct + verify in registers. Straight-line: bits are gathered with
 // constant shifts and reversed once (the packed word is MSB-first).
-__device__ __forceinline__ void finish_image(const DetectParams& p, const CorrSmem& sm, int64_t img,
+__device__ __forceinline__ void finish_image(const DetectParams& p, CorrSmem& sm, int64_t img,
                                              const uint32_t (&acc)[kCorrN]) {
     const int nb = p.nbits;
     uint32_t pos[2] = {0u, 0u}, zer[2] = {0u, 0u};
@@ -94,6 +102,11 @@ __device__ __forceinline__ void finish_image(const DetectParams& p, const CorrSm
         uint64_t cw = 0;
         const int nerr = rs_t1_packed(sm.rs, raw, cw);
         make_record(rec, raw, nerr, cw, nb, p.kbits, p.key_cw, p.key_msg, p.tau_msg, p.tau_raw, 0);
+    } else if (p.fuse_t1) {
+        // tied bits: resolved by the whole CTA after the epilogue (finish_ties)
+        const int slot = atomicAdd(&sm.nties, 1);
+        sm.ties[slot] = CorrSmem::TieEntry{img, tmask, raw};
+        return;
     } else {
         rec.raw = raw;
         rec.msg = 0;
@@ -106,6 +119,58 @@ __device__ __forceinline__ void finish_image(const DetectParams& p, const CorrSm
         p.pending[slot] = PendingEntry{img, tmask};
     }
     store_record(p.out + img, rec);
+}
+
+// Exact reference hard bit of a zero integer correlation. The reference sums
+// double(float(v/127.5 - 1)) * P sequentially (stego.cpp:60-64) and tests
+// soft > 0 (stego.cpp:12). Every term is a multiple of 2^-31 (the float ulp at
+// |d| >= 1/255) and |sum| < 2^16, so every partial sum is exact in double and
+// the reference's result is the exact sum: an int64 dot product of the window
+// with P through the table lut[v] = d(v) * 2^31, in any order (lane-parallel).
+__device__ __forceinline__ bool tie_bit_exact(const WindowSource& s, int64_t img, int K, const int8_t* pat,
+                                              const long long* lut, int lane) {
+    const uint8_t* wb = window_base(s, img, K);
+    const int row_bytes = 3 * s.l;
+    const int pitch = s.direct ? s.pitch : row_bytes;
+    long long acc = 0;
+    for (int px = lane; px < K; px += 32) {
+        const int trow = px / row_bytes;
+        const long long d = lut[wb[static_cast<int64_t>(trow) * pitch + (px - trow * row_bytes)]];
+        acc += pat[px] > 0 ? d : -d;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    return acc > 0;
+}
+
+// t = 1 codes: the CTA's images with tied bits (collected by finish_image),
+// one warp per image — resolve the tied bits, then RS + verify + record.
+__device__ __noinline__ void finish_ties(const DetectParams& p, CorrSmem& sm, int warp, int lane) {
+    for (int v = threadIdx.x; v < 256; v += kCorrThreads) {
+        const float d = __double2float_rn(__dsub_rn(__ddiv_rn(static_cast<double>(v), 127.5), 1.0));
+        sm.tie_lut[v] = __double2ll_rn(static_cast<double>(d) * 2147483648.0);
+    }
+    __syncthreads();
+    griddep_wait();  // the previous grid is done with the records
+    const int nb = p.nbits;
+    for (int e = warp; e < sm.nties; e += kCorrThreads / 32) {
+        const CorrSmem::TieEntry te = sm.ties[e];
+        uint64_t raw = te.raw;
+        for (uint64_t m = te.tie_mask; m; m &= m - 1) {
+            const int b = __ffsll(static_cast<long long>(m)) - 1;
+            if (tie_bit_exact(p.src, te.image, p.K, p.patterns + static_cast<int64_t>(b) * p.K_pad, sm.tie_lut, lane))
+                raw |= 1ull << (nb - 1 - b);
+        }
+        if (lane == 0) {
+            if (p.raw_out) p.raw_out[te.image] = raw;
+            uint64_t cw = 0;
+            const int nerr = rs_t1_packed(sm.rs, raw, cw);
+            qrm_record rec;
+            make_record(rec, raw, nerr, cw, nb, p.kbits, p.key_cw, p.key_msg, p.tau_msg, p.tau_raw,
+                        __popcll(te.tie_mask));
+            store_record(p.out + te.image, rec);
+        }
+    }
 }
 
 // Launched as clusters of S = 1, 2 or 4 CTAs along K (split-K): CTA r of a
@@ -137,6 +202,7 @@ __global__ void __launch_bounds__(kCorrThreads, 1) corr_detect_kernel(const __gr
         }
         mbar_init(&sm.accum_full, 1);
         mbar_fence_init();
+        sm.nties = 0;
     }
     griddep_launch_dependents();  // the completion kernel may launch; it waits for this grid
     if (tid < kCorrN) sm.thr[tid] = 255 * __ldg(p.colsum + tid);
@@ -284,6 +350,7 @@ __global__ void __launch_bounds__(kCorrThreads, 1) corr_detect_kernel(const __gr
     }
     dbg_mark(p, 7, tid);
     __syncthreads();
+    if (sm.nties > 0) finish_ties(p, sm, warp, lane);  // rare: exact zero correlations
     if (warp == 4) {
         tc_fence_after();
         tmem_dealloc<kCorrN>(tmem);
