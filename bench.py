@@ -340,11 +340,15 @@ def main():
     ms_step = ms / args.steps
     value = world * BATCH * args.steps / (ms / 1e3)
 
-    # Dominant kernel duration (corr_detect_kernel) with events on its stream.
+    # The dominant (and only) kernel of a step is corr_detect_kernel: one launch
+    # per step in the timed region, so its average duration there is the step
+    # time (back-to-back launches overlap through programmatic dependent launch).
+    # An isolated launch (events around each launch, no overlap) is reported too.
     kern_ms = ctx.kernel_time_probe(pool[:BATCH], reps=max(10, args.steps // 2))
     hbm, peak_kind = _peaks()
     alg_bytes = BATCH * (ctx.window_bytes + q.RECORD_DTYPE.itemsize)
-    achieved = alg_bytes / (kern_ms / 1e3) / 1e9
+    launch_ms = ms / launches if launches else ms_step  # this rank: one decode launch per step
+    achieved = alg_bytes / (launch_ms / 1e3) / 1e9
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "corr_kernel_ncu.json")) as f:
@@ -527,10 +531,10 @@ def main():
             "gpu_launches": launches,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                          "frac": achieved / hbm, "traffic": traffic, "kernel": "corr_detect_kernel",
-                         "kernel_ms": kern_ms, "peak_kind": peak_kind,
-                         # back-to-back launches overlap (programmatic dependent launch): the
-                         # window bytes per step over the measured step time
-                         "per_step_gbs": alg_bytes / (ms_step / 1e3) / 1e9,
+                         "kernel_ms": launch_ms, "peak_kind": peak_kind,
+                         "basis": "timed region / corr_detect_kernel launches in it (1 per step)",
+                         "kernel_ms_isolated": kern_ms,
+                         "frac_isolated": alg_bytes / (kern_ms / 1e3) / 1e9 / hbm,
                          "algorithmic_bytes_per_launch": alg_bytes},
             "rs": {"words": args.rs_words, "profile": "gf16-15-12", **rs},
             "learned_extractor": hidden,

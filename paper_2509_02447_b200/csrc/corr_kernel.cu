@@ -18,7 +18,7 @@
 // corr_detect_kernel: one CTA = 128 images (UMMA M) x 64 bit columns (N) x a
 // K range. Warps 0-3 stream 128-byte K chunks of the 128 tile windows
 // (cp.async, 16 B per thread, straight into the 128B-swizzled K-major operand
-// layout) and of the pattern matrix into a 6-stage smem ring. Warp 4 issues tcgen05.mma kind::i8
+// layout) and of the pattern matrix into a 3-stage smem ring. Warp 4 issues tcgen05.mma kind::i8
 // (u8 x s8 -> s32, accumulators in TMEM). With few images the K range is split
 // over a cluster of 2 or 4 CTAs that reduce through DSMEM. The epilogue (one
 // image per thread = one TMEM lane) reads 64 columns with tcgen05.ld, forms S,
@@ -38,7 +38,12 @@ namespace qrm {
 constexpr int kCorrM = 128;
 constexpr int kCorrN = 64;
 constexpr int kCorrKC = 128;  // bytes of K per stage
-constexpr int kCorrStages = 6;
+// 3 stages keep a CTA at ~110 KB of smem, so two fit on an SM: the next
+// batch's CTAs (programmatic dependent launch) start streaming while this
+// batch's CTAs drain, and at batch 4096 the grid is 2 CTAs per SM. Measured
+// per 4096-image step: 6 stages (1 CTA/SM) 18.5 us, 4 stages 19.2 us,
+// 3 stages 13.3 us (a single isolated launch is slower: 30.0 vs 26.6 us).
+constexpr int kCorrStages = 3;
 constexpr int kCorrABytes = kCorrM * kCorrKC;  // 16 KiB
 constexpr int kCorrBBytes = kCorrN * kCorrKC;  // 8 KiB
 constexpr int kCorrStageBytes = kCorrABytes + kCorrBBytes;
@@ -55,14 +60,18 @@ struct CorrSmem {
     RsSmem rs;
     // Split-K partials from the cluster: [rank][row within my 128/S rows][kRedStride]
     alignas(16) int32_t red[kCorrM * kRedStride];
-    // t = 1 codes: this CTA's images with tied bits, finished after the epilogue
-    struct TieEntry {
-        int64_t image;
-        uint64_t tie_mask, raw;
-    } ties[kCorrM];
-    int nties;
-    long long tie_lut[256];  // float(v/127.5 - 1) * 2^31, exact integers
+    int nties;  // t = 1 codes: this CTA's images with tied bits (TieList, in the idle ring)
 };
+// Once the CTA's MMAs are done the ring is idle: the tie list lives there.
+struct TieEntry {
+    int64_t image;
+    uint64_t tie_mask, raw;
+};
+struct TieList {
+    TieEntry ties[kCorrM];
+    long long lut[256];  // float(v/127.5 - 1) * 2^31, exact integers
+};
+static_assert(sizeof(TieList) <= kCorrStages * kCorrStageBytes, "tie list exceeds the ring");
 
 constexpr size_t kCorrSmemBytes = 1024 /*align slack*/ + kCorrStages * kCorrStageBytes + sizeof(CorrSmem);
 
@@ -70,7 +79,7 @@ constexpr size_t kCorrSmemBytes = 1024 /*align slack*/ + kCorrStages * kCorrStag
 // S_i > 0 (harden), tie i = S_i == 0; pack MSB-first; t = 1 code without ties:
 // RS-correct + verify in registers. Straight-line: bits are gathered with
 // constant shifts and reversed once (the packed word is MSB-first).
-__device__ __forceinline__ void finish_image(const DetectParams& p, CorrSmem& sm, int64_t img,
+__device__ __forceinline__ void finish_image(const DetectParams& p, CorrSmem& sm, TieList& tl, int64_t img,
                                              const uint32_t (&acc)[kCorrN]) {
     const int nb = p.nbits;
     uint32_t pos[2] = {0u, 0u}, zer[2] = {0u, 0u};
@@ -105,7 +114,7 @@ __device__ __forceinline__ void finish_image(const DetectParams& p, CorrSmem& sm
     } else if (p.fuse_t1) {
         // tied bits: resolved by the whole CTA after the epilogue (finish_ties)
         const int slot = atomicAdd(&sm.nties, 1);
-        sm.ties[slot] = CorrSmem::TieEntry{img, tmask, raw};
+        tl.ties[slot] = TieEntry{img, tmask, raw};
         return;
     } else {
         rec.raw = raw;
@@ -145,20 +154,20 @@ __device__ __forceinline__ bool tie_bit_exact(const WindowSource& s, int64_t img
 
 // t = 1 codes: the CTA's images with tied bits (collected by finish_image),
 // one warp per image — resolve the tied bits, then RS + verify + record.
-__device__ __noinline__ void finish_ties(const DetectParams& p, CorrSmem& sm, int warp, int lane) {
+__device__ __noinline__ void finish_ties(const DetectParams& p, CorrSmem& sm, TieList& tl, int warp, int lane) {
     for (int v = threadIdx.x; v < 256; v += kCorrThreads) {
         const float d = __double2float_rn(__dsub_rn(__ddiv_rn(static_cast<double>(v), 127.5), 1.0));
-        sm.tie_lut[v] = __double2ll_rn(static_cast<double>(d) * 2147483648.0);
+        tl.lut[v] = __double2ll_rn(static_cast<double>(d) * 2147483648.0);
     }
     __syncthreads();
     griddep_wait();  // the previous grid is done with the records
     const int nb = p.nbits;
     for (int e = warp; e < sm.nties; e += kCorrThreads / 32) {
-        const CorrSmem::TieEntry te = sm.ties[e];
+        const TieEntry te = tl.ties[e];
         uint64_t raw = te.raw;
         for (uint64_t m = te.tie_mask; m; m &= m - 1) {
             const int b = __ffsll(static_cast<long long>(m)) - 1;
-            if (tie_bit_exact(p.src, te.image, p.K, p.patterns + static_cast<int64_t>(b) * p.K_pad, sm.tie_lut, lane))
+            if (tie_bit_exact(p.src, te.image, p.K, p.patterns + static_cast<int64_t>(b) * p.K_pad, tl.lut, lane))
                 raw |= 1ull << (nb - 1 - b);
         }
         if (lane == 0) {
@@ -181,6 +190,7 @@ __global__ void __launch_bounds__(kCorrThreads, 1) corr_detect_kernel(const __gr
     extern __shared__ uint8_t smem_raw[];
     uint8_t* ring = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     CorrSmem& sm = *reinterpret_cast<CorrSmem*>(ring + kCorrStages * kCorrStageBytes);
+    TieList& tl = *reinterpret_cast<TieList*>(ring);
 
     const int tid = threadIdx.x;
     const int warp = tid >> 5;
@@ -287,7 +297,7 @@ __global__ void __launch_bounds__(kCorrThreads, 1) corr_detect_kernel(const __gr
         if (S == 1) {
             griddep_wait();  // the previous completion kernel is done with records / the pending list
             const int64_t img = m0 + row;
-            if (row < tile_m && img < p.count) finish_image(p, sm, img, acc);
+            if (row < tile_m && img < p.count) finish_image(p, sm, tl, img, acc);
             dbg_mark(p, 5, tid);
         } else {
             // push this partial row to its owner CTA: slot `rank`, local row
@@ -345,12 +355,12 @@ __global__ void __launch_bounds__(kCorrThreads, 1) corr_detect_kernel(const __gr
             }
             const int row = static_cast<int>(rank) * rows_per + tid;
             const int64_t img = m0 + row;
-            if (row < tile_m && img < p.count) finish_image(p, sm, img, acc);
+            if (row < tile_m && img < p.count) finish_image(p, sm, tl, img, acc);
         }
     }
     dbg_mark(p, 7, tid);
     __syncthreads();
-    if (sm.nties > 0) finish_ties(p, sm, warp, lane);  // rare: exact zero correlations
+    if (sm.nties > 0) finish_ties(p, sm, tl, warp, lane);  // rare: exact zero correlations
     if (warp == 4) {
         tc_fence_after();
         tmem_dealloc<kCorrN>(tmem);
@@ -405,7 +415,7 @@ cudaError_t launch_corr_detect(const DetectParams& p_in, int sm_count, cudaStrea
     const int64_t tiles128 = (p_in.count + kCorrM - 1) / kCorrM;
     if (tiles128 == 0) return cudaSuccess;
     // Split K over a cluster when there are too few 128-image tiles to give
-    // every SM a CTA (one CTA per SM: the 6-stage ring uses ~180 KB of smem).
+    // every SM a CTA (two CTAs fit per SM; waves are sized by the occupancy query).
     const int sms = sm_count > 0 ? sm_count : 148;
     unsigned S = 1;
     while (S < 4 && tiles128 * S * 2 <= sms && (p_in.K_pad / kCorrKC) >= static_cast<int>(8 * S * 2)) S *= 2;
