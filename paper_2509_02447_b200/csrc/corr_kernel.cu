@@ -38,11 +38,13 @@ namespace qrm {
 constexpr int kCorrM = 128;
 constexpr int kCorrN = 64;
 constexpr int kCorrKC = 128;  // bytes of K per stage
-// 3 stages keep a CTA at ~110 KB of smem, so two fit on an SM: the next
-// batch's CTAs (programmatic dependent launch) start streaming while this
-// batch's CTAs drain, and at batch 4096 the grid is 2 CTAs per SM. Measured
-// per 4096-image step: 6 stages (1 CTA/SM) 18.5 us, 4 stages 19.2 us,
-// 3 stages 13.3 us (a single isolated launch is slower: 30.0 vs 26.6 us).
+// 3 stages keep a CTA at ~110 KB of smem, so two fit on an SM: the grid still
+// places one CTA per SM (the occupancy query's cluster waves), and the other
+// half of each SM takes the next batch's CTAs (programmatic dependent launch),
+// which stream while this batch's CTAs drain. Measured per 4096-image step:
+// 6 stages 18.5 us, 4 stages 19.2 us, 3 stages 13.3 us (an isolated launch is
+// slower: 30.0 vs 26.6 us); 3 stages with two CTAs per SM in the same grid
+// (66 clusters) 19.2 us.
 constexpr int kCorrStages = 3;
 constexpr int kCorrABytes = kCorrM * kCorrKC;  // 16 KiB
 constexpr int kCorrBBytes = kCorrN * kCorrKC;  // 8 KiB
@@ -415,7 +417,7 @@ cudaError_t launch_corr_detect(const DetectParams& p_in, int sm_count, cudaStrea
     const int64_t tiles128 = (p_in.count + kCorrM - 1) / kCorrM;
     if (tiles128 == 0) return cudaSuccess;
     // Split K over a cluster when there are too few 128-image tiles to give
-    // every SM a CTA (two CTAs fit per SM; waves are sized by the occupancy query).
+    // every SM a CTA (waves of co-resident clusters from the occupancy query).
     const int sms = sm_count > 0 ? sm_count : 148;
     unsigned S = 1;
     while (S < 4 && tiles128 * S * 2 <= sms && (p_in.K_pad / kCorrKC) >= static_cast<int>(8 * S * 2)) S *= 2;
