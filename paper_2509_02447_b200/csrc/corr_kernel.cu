@@ -18,7 +18,7 @@
 // corr_detect_kernel: one CTA = 128 images (UMMA M) x 64 bit columns (N) x a
 // K range. Warps 0-3 stream 128-byte K chunks of the 128 tile windows
 // (cp.async, 16 B per thread, straight into the 128B-swizzled K-major operand
-// layout) and of the pattern matrix into a 3-stage smem ring. Warp 4 issues tcgen05.mma kind::i8
+// layout) and of the pattern matrix into a 4-stage smem ring. Warp 4 issues tcgen05.mma kind::i8
 // (u8 x s8 -> s32, accumulators in TMEM). With few images the K range is split
 // over a cluster of 2 or 4 CTAs that reduce through DSMEM. The epilogue (one
 // image per thread = one TMEM lane) reads 64 columns with tcgen05.ld, forms S,
@@ -38,14 +38,17 @@ namespace qrm {
 constexpr int kCorrM = 128;
 constexpr int kCorrN = 64;
 constexpr int kCorrKC = 128;  // bytes of K per stage
-// 3 stages keep a CTA at ~110 KB of smem, so two fit on an SM: the grid still
-// places one CTA per SM (the occupancy query's cluster waves), and the other
-// half of each SM takes the next batch's CTAs (programmatic dependent launch),
-// which stream while this batch's CTAs drain. Measured per 4096-image step:
-// 6 stages 18.5 us, 4 stages 19.2 us, 3 stages 13.3 us (an isolated launch is
-// slower: 30.0 vs 26.6 us); 3 stages with two CTAs per SM in the same grid
-// (66 clusters) 19.2 us.
-constexpr int kCorrStages = 3;
+// A 4-stage ring, with the end-of-kernel buffers (split-K partials, tie list)
+// aliased into it, keeps a CTA at ~99 KB of smem, so two fit on an SM. The
+// grid still places one CTA per SM (the occupancy query's cluster waves); the
+// other half of each SM takes the next batch's CTAs (programmatic dependent
+// launch), which stream while this batch's CTAs run their tails. Measured per
+// 4096-image step, back to back: 6 stages (one CTA per SM) 18.5 us; 4 stages
+// 13.0 us; 3 stages (three CTAs per SM) 13.5 us but the host pipeline's
+// transfer kernel then ran erratically beside the decode grids (configs[4]
+// 0.5-3.1 M img/s vs 3.6); two CTAs per SM from one batch (66 clusters)
+// 19.2 us. An isolated launch is slower (27.5 vs 26.6 us at 6 stages).
+constexpr int kCorrStages = 4;
 constexpr int kCorrABytes = kCorrM * kCorrKC;  // 16 KiB
 constexpr int kCorrBBytes = kCorrN * kCorrKC;  // 8 KiB
 constexpr int kCorrStageBytes = kCorrABytes + kCorrBBytes;
@@ -60,11 +63,12 @@ struct CorrSmem {
     uint32_t tmem_base;
     alignas(16) int32_t thr[kCorrN];  // 255 * colsum(P_i): bit i = 2 D_i > thr_i
     RsSmem rs;
-    // Split-K partials from the cluster: [rank][row within my 128/S rows][kRedStride]
-    alignas(16) int32_t red[kCorrM * kRedStride];
-    int nties;  // t = 1 codes: this CTA's images with tied bits (TieList, in the idle ring)
+    int nties;  // t = 1 codes: this CTA's images with tied bits (TieList)
 };
-// Once the CTA's MMAs are done the ring is idle: the tie list lives there.
+// Once every MMA of the cluster is done the rings are idle, and the end-of-
+// kernel buffers live there: the split-K partials pushed by the cluster,
+// red[rank][row within my 128/S rows][kRedStride] (ring offset 0), then the
+// tie list.
 struct TieEntry {
     int64_t image;
     uint64_t tie_mask, raw;
@@ -73,7 +77,8 @@ struct TieList {
     TieEntry ties[kCorrM];
     long long lut[256];  // float(v/127.5 - 1) * 2^31, exact integers
 };
-static_assert(sizeof(TieList) <= kCorrStages * kCorrStageBytes, "tie list exceeds the ring");
+constexpr int kRedBytes = kCorrM * kRedStride * 4;
+static_assert(kRedBytes + sizeof(TieList) <= kCorrStages * kCorrStageBytes, "end-of-kernel buffers exceed the ring");
 
 constexpr size_t kCorrSmemBytes = 1024 /*align slack*/ + kCorrStages * kCorrStageBytes + sizeof(CorrSmem);
 
@@ -192,7 +197,8 @@ __global__ void __launch_bounds__(kCorrThreads, 1) corr_detect_kernel(const __gr
     extern __shared__ uint8_t smem_raw[];
     uint8_t* ring = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     CorrSmem& sm = *reinterpret_cast<CorrSmem*>(ring + kCorrStages * kCorrStageBytes);
-    TieList& tl = *reinterpret_cast<TieList*>(ring);
+    int32_t* red = reinterpret_cast<int32_t*>(ring);
+    TieList& tl = *reinterpret_cast<TieList*>(ring + kRedBytes);
 
     const int tid = threadIdx.x;
     const int warp = tid >> 5;
@@ -305,7 +311,11 @@ __global__ void __launch_bounds__(kCorrThreads, 1) corr_detect_kernel(const __gr
             // push this partial row to its owner CTA: slot `rank`, local row
             const uint32_t owner = static_cast<uint32_t>(row / rows_per);
             const uint32_t local = static_cast<uint32_t>(row % rows_per);
-            const uint32_t dst = map_to_rank(smem_u32(&sm.red[(rank * rows_per + local) * kRedStride]), owner);
+            // the owner's ring takes the partials: wait until every MMA of the
+            // cluster is done (each CTA's producers passed its accum_full)
+            cluster_arrive();
+            cluster_wait();
+            const uint32_t dst = map_to_rank(smem_u32(&red[(rank * rows_per + local) * kRedStride]), owner);
 #pragma unroll
             for (int q = 0; q < kCorrN / 4; ++q)
                 st_cluster_v4(dst + 16 * q, acc[4 * q], acc[4 * q + 1], acc[4 * q + 2], acc[4 * q + 3]);
@@ -335,6 +345,10 @@ __global__ void __launch_bounds__(kCorrThreads, 1) corr_detect_kernel(const __gr
             umma_commit(&sm.accum_full);
         }
         __syncwarp();
+        if (S > 1) {  // the producers' "all MMAs done" cluster barrier phase
+            cluster_arrive();
+            cluster_wait();
+        }
     }
     if (S > 1) {
         cluster_sync_all();  // every partial row has landed in its owner's smem
@@ -345,7 +359,7 @@ __global__ void __launch_bounds__(kCorrThreads, 1) corr_detect_kernel(const __gr
 #pragma unroll
             for (int i = 0; i < kCorrN; ++i) acc[i] = 0;
             for (uint32_t s = 0; s < S; ++s) {
-                const int4* src = reinterpret_cast<const int4*>(&sm.red[(s * rows_per + tid) * kRedStride]);
+                const int4* src = reinterpret_cast<const int4*>(&red[(s * rows_per + tid) * kRedStride]);
 #pragma unroll
                 for (int q = 0; q < kCorrN / 4; ++q) {
                     const int4 v = src[q];
