@@ -89,6 +89,21 @@ def test_ties_resolved_bit_exactly(qrm, cuda, ref, cfg):
         assert bool(Ri["verified"][0]) == bool(rec["verified"][i])
 
 
+@pytest.mark.parametrize("ksplit", ["1", "2", "4"])
+def test_ties_same_across_split_k(qrm, cuda, cfg, monkeypatch, ksplit):
+    """The decode kernel resolves tied bits in-CTA; with split-K the partial
+    rows and the tie list live in the idle operand ring. Records (ties
+    included) must not depend on the split (the default is checked against
+    the reference above)."""
+    imgs = qrm.make_corpus(cfg, 90000, 2048, embed=False)
+    with qrm.DetectionContext(cfg) as ctx:
+        base = qrm.records_from_device(ctx.detect_device(imgs))
+        monkeypatch.setenv("QRM_CORR_KSPLIT", ksplit)
+        rec = qrm.records_from_device(ctx.detect_device(imgs))
+    assert (base["ties"] > 0).any()
+    assert np.array_equal(rec.view(np.uint8), base.view(np.uint8))
+
+
 def test_soft_values_match_reference(qrm, cuda, ref, cfg):
     """GPU soft = S / (255 K), exact. The reference sums float32-rounded samples
     float(v/127.5 - 1) in double, so |ref - exact| <= max_v |float(v/127.5-1) -
