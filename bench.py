@@ -453,7 +453,7 @@ def main():
             ctx.extract_tiles(pool[(i % nb) * BATCH:(i % nb + 1) * BATCH], first_draw=i * BATCH, out=tiles_out)
         torch.cuda.synchronize()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        reps = 20
+        reps = 60
         a.record(stream)
         for i in range(reps):
             ctx.extract_tiles(pool[(i % nb) * BATCH:(i % nb + 1) * BATCH], first_draw=i * BATCH, out=tiles_out)

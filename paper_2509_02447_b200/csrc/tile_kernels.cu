@@ -40,6 +40,7 @@ __global__ void __launch_bounds__(kTbThreads) tile_bf16_kernel(const __grid_cons
         mbar_fence_init();
     }
     __syncthreads();
+    griddep_launch_dependents();  // the next launch's prologue and first loads may overlap this one
     auto issue = [&](int64_t t, int buf) {
         int x0 = 0, y0 = 0;
         if (p.src.direct) {
@@ -59,6 +60,7 @@ __global__ void __launch_bounds__(kTbThreads) tile_bf16_kernel(const __grid_cons
         // the other buffer was fully consumed before the previous iteration's barrier
         if (tid == 0 && t + gridDim.x < p.count) issue(t + gridDim.x, buf ^ 1);
         mbar_wait(&full[buf], (i >> 1) & 1);
+        if (i == 0) griddep_wait();  // the previous launch is done with the output
         const uint8_t* w = win[buf];
         if (p.channels == 4) {
             // 2 pixels (6 bytes -> 16 B) per 16-B store; 2048 stores per tile
@@ -87,8 +89,16 @@ cudaError_t launch_tile_bf16(const CUtensorMap& tmap, const TileBf16Params& p, i
     if (p.count <= 0) return cudaSuccess;
     int64_t grid = static_cast<int64_t>(sm_count > 0 ? sm_count : 148) * 8;
     if (grid > p.count) grid = p.count;
-    tile_bf16_kernel<<<static_cast<unsigned>(grid), kTbThreads, 0, st>>>(tmap, p);
-    return cudaGetLastError();
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(static_cast<unsigned>(grid));
+    cfg.blockDim = dim3(kTbThreads);
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // programmatic dependent launch
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, tile_bf16_kernel, tmap, p);
 }
 
 }  // namespace qrm
