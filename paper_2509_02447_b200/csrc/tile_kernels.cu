@@ -17,6 +17,7 @@
 
 #include "qrm_device.cuh"
 #include "qrm_types.h"
+#include "qrm_window.cuh"
 
 namespace qrm {
 
@@ -83,6 +84,56 @@ __global__ void __launch_bounds__(kTbThreads) tile_bf16_kernel(const __grid_cons
         }
         __syncthreads();  // every thread is done with win[buf] before it is refilled
     }
+}
+
+// fetch_windows_tma_kernel — the host pipeline's transfer stage with TMA: one
+// 3-D box (64 rows x 192 B) per image read straight from mapped pinned host
+// memory into shared memory, then one bulk copy of the 12 KB window to its
+// slot in HBM. One thread per CTA drives kFtBuf windows in flight.
+constexpr int kFtBuf = 3;
+__global__ void __launch_bounds__(32) fetch_windows_tma_kernel(const __grid_constant__ CUtensorMap tmap,
+                                                               const __grid_constant__ WindowSource src, int64_t count,
+                                                               uint8_t* __restrict__ out) {
+    __shared__ __align__(128) uint8_t win[kFtBuf][kTbWin];
+    __shared__ __align__(8) uint64_t full[kFtBuf];
+    if (threadIdx.x != 0) return;
+    for (int b = 0; b < kFtBuf; ++b) mbar_init(&full[b], 1);
+    mbar_fence_init();
+    auto issue = [&](int64_t t, int b) {
+        int tx, ty;
+        select_tile(kWorkingSize, kWorkingSize, src.l, src.strategy, src.tile_seed,
+                    src.first_draw + static_cast<uint64_t>(t), tx, ty);
+        mbar_arrive_expect_tx(&full[b], kTbWin);
+        tma_load_3d(smem_u32(win[b]), &tmap, (src.x_off + tx) * 3, src.y_off + ty, static_cast<int>(t), &full[b]);
+    };
+    const int64_t g = gridDim.x;
+    for (int b = 0; b < kFtBuf && blockIdx.x + b * g < count; ++b) issue(blockIdx.x + b * g, b);
+    int i = 0;
+    for (int64_t t = blockIdx.x; t < count; t += g, ++i) {
+        const int b = i % kFtBuf;
+        mbar_wait(&full[b], (i / kFtBuf) & 1);
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(out + t * kTbWin),
+                     "r"(smem_u32(win[b])), "r"(kTbWin)
+                     : "memory");
+        bulk_commit();
+        const int64_t tn = t + kFtBuf * g;
+        if (tn < count) {
+            bulk_wait_read<0>();  // the store has read win[b]
+            issue(tn, b);
+        }
+    }
+    bulk_wait<0>();
+}
+
+cudaError_t launch_fetch_windows_tma(const CUtensorMap& tmap, const WindowSource& src, int64_t count, uint8_t* out,
+                                     int sm_count, cudaStream_t st) {
+    if (count <= 0) return cudaSuccess;
+    // one CTA (one thread, 3 windows in flight) per SM already fills the link
+    // (1, 2, 4 or 8 per SM measured the same); the decode kernel keeps the SMs
+    int64_t grid = sm_count > 0 ? sm_count : 148;
+    if (grid > count) grid = count;
+    fetch_windows_tma_kernel<<<static_cast<unsigned>(grid), 32, 0, st>>>(tmap, src, count, out);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_tile_bf16(const CUtensorMap& tmap, const TileBf16Params& p, int sm_count, cudaStream_t st) {
