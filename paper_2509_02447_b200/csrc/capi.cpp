@@ -1243,11 +1243,15 @@ qrm_status encode_act_tmap(CUtensorMap* map, CUtensorMap* store_map, void* base,
 // One 64->64 conv layer: the CTA-pair kernel (cta_group::2, M = 256; 237 us per
 // 1024 tiles against 285 us for the single-CTA kernel); QRM_CONV_PAIR=0 selects
 // the single-CTA variant.
+// The CTA-pair conv layer is the default; QRM_CONV_PAIR=0 selects the single-CTA one.
+bool conv_pair_enabled() {
+    const char* e = getenv("QRM_CONV_PAIR");
+    return !(e && e[0] == '0');
+}
+
 cudaError_t conv64_layer(const CUtensorMap& tmap, const CUtensorMap& tmap_out, const HiddenLayerParams& p, int sms,
                          cudaStream_t st) {
-    const char* e = getenv("QRM_CONV_PAIR");
-    const bool pair = !(e && e[0] == '0');
-    return pair ? launch_conv64_pair(tmap, tmap_out, p, sms, st) : launch_conv64(tmap, tmap_out, p, sms, st);
+    return conv_pair_enabled() ? launch_conv64_pair(tmap, tmap_out, p, sms, st) : launch_conv64(tmap, tmap_out, p, sms, st);
 }
 
 qrm_status hidden_prepare(qrm_ctx* c, uint64_t seed, int64_t tiles, cudaStream_t st) {
@@ -1304,6 +1308,11 @@ qrm_status hidden_run(qrm_ctx* c, Workspace& W, const WindowSource& src, int64_t
     for (int64_t off = 0; off < count; off += kConvChunk) {
         const int64_t n = std::min(kConvChunk, count - off);
         const WindowSource cs = slice_source(src, off, c->K);
+        const bool pair = conv_pair_enabled();
+        // the pair kernel's last layer folds the linear layer into its epilogue
+        // (QRM_CONV_FUSE_LINEAR=0: channel partials + hidden_head_kernel instead)
+        const char* fl = getenv("QRM_CONV_FUSE_LINEAR");
+        const bool fuse_linear = pair && !(fl && fl[0] == '0');
         Conv0Params p0{cs, n, c->K, H.w0, H.bias, H.act[0]};
         QRM_LAUNCH(launch_conv0(p0, H.tmap_st[0], c->sms, st));
         for (int j = 1; j < kHiddenLayers; ++j) {
@@ -1314,6 +1323,11 @@ qrm_status hidden_run(qrm_ctx* c, Workspace& W, const WindowSource& src, int64_t
             lp.act_out = lp.last ? nullptr : H.act[j & 1];
             lp.pool_out = lp.last ? H.pool : nullptr;
             lp.tiles = n;
+            if (lp.last && fuse_linear) {
+                lp.fuse_linear = 1;
+                lp.wl = H.wl;
+                lp.nbits = c->nbits;
+            }
             QRM_LAUNCH(conv64_layer(H.tmap[(j - 1) & 1], H.tmap_st[j & 1], lp, c->sms, st));
         }
         HeadParams hp{};
@@ -1333,7 +1347,8 @@ qrm_status hidden_run(qrm_ctx* c, Workspace& W, const WindowSource& src, int64_t
         hp.out = out + off;
         hp.pending_count = W.pending_count;
         hp.pending = W.pending;
-        QRM_LAUNCH(launch_hidden_head(hp, st));
+        if (fuse_linear) QRM_LAUNCH(launch_hidden_sign(hp, st));
+        else QRM_LAUNCH(launch_hidden_head(hp, st));
         DetectParams fp = base_params(c, W, n, out + off, nullptr, nullptr);
         fp.src = cs;
         if (!fp.fuse_t1) QRM_LAUNCH(launch_detect_finish(fp, std::max(1, c->t), c->sms, st));  // general-t codes

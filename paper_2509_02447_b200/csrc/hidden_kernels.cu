@@ -77,7 +77,8 @@ __device__ __forceinline__ void quarter_sync(int q) {
 template <int kSlabs>
 __device__ __forceinline__ void conv_epilogue(const HiddenLayerParams& p, const CUtensorMap* tmap_out,
                                               const uint32_t (&acc)[kHCh], const float* s_bias, float (*pool)[kHC],
-                                              uint32_t o_s, int q, int h, int lane, int64_t tile, int blk, int iter) {
+                                              uint32_t o_s, int q, int h, int lane, int64_t tile, int blk, int iter,
+                                              const float* wl_s = nullptr, float* part_s = nullptr) {
     const int pix = blk * kHM + q * 32 + lane;
     float v[kHCh];
 #pragma unroll
@@ -121,12 +122,32 @@ __device__ __forceinline__ void conv_epilogue(const HiddenLayerParams& p, const 
         }
         pool[q][h * kHCh + lane] = v[0];
         asm volatile("bar.sync 5, 256;" ::: "memory");
-        if (q == 0) {
+        const int c2 = h * kHCh + lane;
+        if (p.fuse_linear) {
+            // linear layer fused: part = the block's channel sums (fixed order);
+            // the block's share of logit o, sum_c wl[o][c] part[c], as four
+            // 16-channel dot products (thread t: o = t % 64, channels 16 (t / 64)
+            // + 0..15; wl_s is [c][o], so a warp's lanes read consecutive o)
+            // added in fixed order. hidden_sign_kernel adds the 32 shares.
+            if (q == 0) part_s[c2] = ((pool[0][c2] + pool[1][c2]) + pool[2][c2]) + pool[3][c2];
+            asm volatile("bar.sync 5, 256;" ::: "memory");
+            const int t = (q + 4 * h + 2) % 8 * 32 + lane;  // 0..255 over the 8 epilogue warps
+            const int o = t & (kHC - 1), g = t >> 6;
+            float s = 0.0f;
+#pragma unroll
+            for (int c = 16 * g; c < 16 * g + 16; ++c) s = fmaf(wl_s[c * kHC + o], part_s[c], s);
+            part_s[kHC + g * kHC + o] = s;
+            asm volatile("bar.sync 5, 256;" ::: "memory");
+            if (g == 0 && o < p.nbits) {
+                const float* sh = part_s + kHC;
+                p.pool_out[(tile * kHBlocks + blk) * kHC + o] = ((sh[o] + sh[kHC + o]) + sh[2 * kHC + o]) + sh[3 * kHC + o];
+            }
+        } else {
             // part 2: fixed-order sum of the 4 quarters -> per-block partial
-            const int c2 = h * kHCh + lane;
-            p.pool_out[(tile * kHBlocks + blk) * kHC + c2] = ((pool[0][c2] + pool[1][c2]) + pool[2][c2]) + pool[3][c2];
+            if (q == 0)
+                p.pool_out[(tile * kHBlocks + blk) * kHC + c2] = ((pool[0][c2] + pool[1][c2]) + pool[2][c2]) + pool[3][c2];
+            asm volatile("bar.sync 5, 256;" ::: "memory");
         }
-        asm volatile("bar.sync 5, 256;" ::: "memory");
     }
 }
 
@@ -276,6 +297,8 @@ struct PairSmem {
     uint64_t acc_full[kHAcc], acc_empty[kHAcc];
     uint32_t tmem_base;
     float pool[4][kHC];
+    float part[5 * kHC];  // fused linear: the block's channel sums, then 4 partial dot products
+    float wl[kHC * kHC];  // fused linear: wl[o][c] at c * 64 + o (conflict-free across o)
 };
 constexpr size_t kPSmemBytes = 1024 + kPWBytes + kPAStages * kHABytes + kPSlabs * kHOBytes + 128 + sizeof(PairSmem);
 static_assert(kPSmemBytes <= 232448, "conv64 pair shared memory exceeds 227 KB");
@@ -311,6 +334,11 @@ __global__ void __launch_bounds__(kHThreads, 1)
         mbar_fence_init();
     }
     if (tid < kHC) s_bias[tid] = p.bias[tid];
+    if (p.fuse_linear)
+        for (int x = tid; x < kHC * kHC; x += kHThreads) {  // zero-padded to 64 x 64
+            const int o = x % kHC, c = x / kHC;
+            sm.wl[x] = (o < p.nbits && c < p.nbits) ? p.wl[o * p.nbits + c] : 0.0f;
+        }
     tc_fence_before();
     cluster_sync_all();  // barriers initialised in both CTAs before any remote arrive
     tc_fence_after();
@@ -390,7 +418,7 @@ __global__ void __launch_bounds__(kHThreads, 1)
             __syncwarp();
             if (lane == 0) mbar_arrive_cluster(empty0[a]);
             conv_epilogue<kPSlabs>(p, &tmap_out, acc, s_bias, sm.pool, o_s, q, h, lane, b / kPairBlocks,
-                                   static_cast<int>(b % kPairBlocks) * 2 + static_cast<int>(rank), i);
+                                   static_cast<int>(b % kPairBlocks) * 2 + static_cast<int>(rank), i, sm.wl, sm.part);
         }
         if (!p.last && h == 0 && lane == 0) bulk_wait<0>();
     }
@@ -614,6 +642,50 @@ __global__ void __launch_bounds__(256) hidden_head_kernel(const __grid_constant_
     }
 }
 
+// Sign: logit o = bl[o] + (sum of the 32 blocks' shares, in block order) / 4096
+// -> hard bits -> (t = 1) RS + verify -> record. One warp per tile.
+__global__ void __launch_bounds__(256) hidden_sign_kernel(const __grid_constant__ HeadParams p) {
+    __shared__ RsSmem T;
+    rs_stage_tables(T, p.rs, threadIdx.x, blockDim.x);
+    __syncthreads();
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t tile = static_cast<int64_t>(blockIdx.x) * 8 + w;
+    if (tile >= p.tiles) return;
+    const int nb = p.nbits;
+    uint64_t raw = 0;
+    for (int o0 = 0; o0 < nb; o0 += 32) {
+        const int o = o0 + lane;
+        float lg = 0.0f;
+        if (o < nb) {
+            const float* sh = p.pool + tile * kHBlocks * kHC + o;
+            float s = 0.0f;
+#pragma unroll 8
+            for (int b = 0; b < kHBlocks; ++b) s += sh[b * kHC];
+            lg = fmaf(s, 1.0f / kHPix, p.bl[o]);
+            if (p.logits) p.logits[tile * nb + o] = lg;
+        }
+        const unsigned bal = __ballot_sync(0xffffffffu, o < nb && lg > 0.0f);
+        raw |= static_cast<uint64_t>(__brev(bal)) << 32 >> o0;  // bit o -> word bit 63 - o
+    }
+    raw >>= (64 - nb);
+    if (lane == 0) {
+        qrm_record rec;
+        if (p.fuse_t1) {
+            uint64_t cw = 0;
+            const int nerr = rs_t1_packed(T, raw, cw);
+            make_record(rec, raw, nerr, cw, nb, p.kbits, p.key_cw, p.key_msg, p.tau_msg, p.tau_raw, 0);
+        } else {
+            rec.raw = raw;
+            rec.msg = 0;
+            rec.status = kRecPending;
+            rec.errors = rec.matches = rec.verified = rec.ties = 0;
+            const int slot = atomicAdd(p.pending_count, 1);
+            p.pending[slot] = PendingEntry{tile, 0};
+        }
+        store_record(p.out + tile, rec);
+    }
+}
+
 // Weight preparation: generate (oracle/hidden_oracle.c formulas), fold BN,
 // write layer j >= 1 as the pre-swizzled bf16 smem image [tap][co][ci].
 __device__ __forceinline__ void hidden_bn(uint64_t seed, int j, int c, float& g, float& be, float& m, float& v) {
@@ -736,6 +808,11 @@ cudaError_t launch_conv64_pair(const CUtensorMap& tmap, const CUtensorMap& tmap_
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     return cudaLaunchKernelEx(&cfg, conv64_pair_kernel, tmap, tmap_out, p);
+}
+
+cudaError_t launch_hidden_sign(const HeadParams& p, cudaStream_t st) {
+    hidden_sign_kernel<<<static_cast<unsigned>((p.tiles + 7) / 8), 256, 0, st>>>(p);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_hidden_head(const HeadParams& p, cudaStream_t st) {

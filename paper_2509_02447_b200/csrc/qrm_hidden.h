@@ -20,6 +20,12 @@ struct HiddenLayerParams {
     float* pool_out;                  // [T][32][64] per-block channel sums (last layer)
     int64_t tiles;
     int last;
+    // Last layer of the pair kernel with the linear layer fused: pool_out[t][b][o]
+    // receives block b's share of logit o, sum_c wl[o][c] * partial_b[c], instead
+    // of the channel partials (hidden_sign_kernel adds the 32 shares in order).
+    int32_t fuse_linear;
+    const float* wl;  // [nbits][nbits]
+    int32_t nbits;
 };
 
 struct Conv0Params {
@@ -56,5 +62,7 @@ cudaError_t launch_conv64(const CUtensorMap& tmap, const CUtensorMap& tmap_out, 
 cudaError_t launch_conv64_pair(const CUtensorMap& tmap, const CUtensorMap& tmap_out, const HiddenLayerParams& p,
                                int sm_count, cudaStream_t st);
 cudaError_t launch_hidden_head(const HeadParams& p, cudaStream_t st);
+// Logits from the last layer's per-block shares (pool = [T][32][64]) -> hard bits -> RS -> records.
+cudaError_t launch_hidden_sign(const HeadParams& p, cudaStream_t st);
 
 }  // namespace qrm
