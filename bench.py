@@ -290,11 +290,11 @@ def main():
     out = torch.empty((BATCH, q.RECORD_DTYPE.itemsize), dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream()
 
+    batches = [pool[b * BATCH:(b + 1) * BATCH] for b in range(nb)]  # views, made once
+
     def step(i):
-        b = i % nb
         # global draw index: weak-scaled shards of one long stream of images
-        first = (i * world + rank) * BATCH
-        ctx.detect_device(pool[b * BATCH:(b + 1) * BATCH], first_draw=first, out=out)
+        ctx.detect_device(batches[i % nb], first_draw=(i * world + rank) * BATCH, out=out)
 
     for i in range(args.warmup):
         step(i)
