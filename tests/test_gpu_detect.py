@@ -211,6 +211,23 @@ def test_host_pipeline_equals_device(qrm, cuda, cfg, mode):
                 ctx.set_transfer_split(1.5)
 
 
+@pytest.mark.parametrize("size", [(512, 512), (320, 272)])
+def test_host_transfer_modes_other_sizes(qrm, cuda, cfg, size):
+    """The transfer stage's TMA window boxes at a centre-crop offset (512^2:
+    x/y offset 128) and on a size whose rows are 16-B aligned but not square;
+    every mode gives the device path's records."""
+    w, h = size
+    imgs = qrm.make_corpus(cfg, 4000, 300, w, h)
+    host = imgs.cpu().numpy()
+    with qrm.DetectionContext(cfg) as ctx:
+        dev = qrm.records_from_device(ctx.detect_device(imgs, first_draw=9))
+        for mode in (0, 1, 2, 3):
+            rec, _ = ctx.detect_host(host, first_draw=9, plan=([1, 2, 1], [128] * 3), mode=mode)
+            assert np.array_equal(rec.view(np.uint8), dev.view(np.uint8)), mode
+    if w == 512:  # the centre crop keeps the embedding grid aligned (offset 128 = 2 tiles)
+        assert dev["verified"].mean() > 0.9
+
+
 @pytest.mark.gpu
 def test_bf16_tiles_match_reference_preprocess(qrm, cuda, ref):
     """North-star item 1: u8 images -> bf16 NHWC tiles equals the reference's
