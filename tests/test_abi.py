@@ -98,3 +98,15 @@ def test_compute_calls_fail_loudly_without_gpu():
         pytest.skip("a GPU is present")
     with pytest.raises(q.CudaError):
         q.DetectionContext(q.DetectionConfig())
+
+
+def test_null_context_calls_report_invalid_input():
+    """Every context entry point validates its handle before touching CUDA, so
+    the reference's InvalidInput convention holds without a device."""
+    import ctypes as C
+    L = q.lib()
+    invalid = 1  # QRM_INVALID_INPUT (include/qrmark_gpu.h)
+    assert L.qrm_ctx_set_transfer_split(None, C.c_double(0.5)) == invalid
+    assert L.qrm_ctx_set_extractor(None, 0, 7) == invalid
+    assert L.qrm_detect_device(None, None, 0, 256, 256, 196608, 0, None, None) == invalid
+    assert "null context" in L.qrm_last_error().decode()
