@@ -363,7 +363,7 @@ def main():
     # records land in pinned host memory (a pageable buffer would be registered per call)
     recs_pin = torch.empty((BATCH, q.RECORD_DTYPE.itemsize), dtype=torch.uint8, pin_memory=True)
     recs_h = recs_pin.numpy().view(q.RECORD_DTYPE).reshape(-1)
-    plan = ([1, 2, 1], [BATCH // 2] * 3)
+    plan = ([1, 2, 1], [BATCH] * 3)  # the context's default plan (one mini-batch per 4096-image call)
 
     nb_host = (POOL // 2) // BATCH
 
