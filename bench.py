@@ -112,10 +112,31 @@ def cpu_reference_run(steps: int, warmup: int, sample: int, threads: int | None 
         _, wall_ns = ref.detect_batch(list(imgs), cfg, plan=plan, rs_workers=nproc, records=False)
         if i >= warmup:
             rates.append(sample / (wall_ns / 1e9))
-    info = {"cores": nproc, "kind": "reference",
+    info = {"cores": nproc, "kind": "reference", "cpu_model": cpu_model(),
             "sample": f"{sample} images 256x256 (cmd_bench corpus), reference detect_batch with plan "
                       f"streams={plan[0]} on {nproc} host threads, median of {steps} runs"}
     return rates, info
+
+
+def cpu_model() -> str:
+    """The host CPU (BASELINE.md 3.5 asks for the lscpu model name)."""
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def bench_config(world: int) -> dict:
+    """The workload both arms run (identical dicts, so the driver's same_config holds)."""
+    return {"workload": "configs[1]: 256x256 RGB batch 4096 per GPU, one 64x64 tile/image (random_grid), "
+                        "spread-spectrum decoder (60 bits) + gf16-15-12 RS + verify",
+            "global_batch": BATCH * world, "per_gpu_batch": BATCH, "parallelism": f"dp{world} (image shards)",
+            "l2": "inputs rotate over a 16,384-image pool (3.2 GB; each step a different batch and draw range, "
+                  "4 x 50 MB of tile windows per rotation > 126 MB L2)"}
 
 
 def cpu_rs_baseline(words_np, threads):
@@ -137,17 +158,43 @@ def run_reference_arm(args):
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f32/f64 (reference CPU)", "data": "synthetic",
             "impl": "reference",
-            "config": {"workload": "configs[1]: 256x256 RGB, one 64x64 tile/image, gf16-15-12 RS, batch 4096 "
-                                   "(reference runs a bounded sample per step)", "global_batch": BATCH,
-                       "image": [H, W, 3], "tile": 64, "profile": "gf16-15-12"},
+            "config": bench_config(world),
             "cpu_baseline": {"value": value, "unit": "images/s", "cores": info["cores"], "kind": info["kind"],
-                             "sample": info["sample"]},
+                             "cpu_model": info["cpu_model"],
+                             "sample": info["sample"] + " (a bounded sample of the workload per step)"},
             "e2e": {"value": value, "unit": "images/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
 
 
 HIDDEN_FLOP_PER_TILE = 2 * 64 * 64 * (27 * 64 + 7 * 576 * 64 + 576 * 60) + 2 * 60 * 60
+
+
+def dropin_submetric(images_np, args, device):
+    """Builds and runs tests/cpp/bench_dropin.cpp (g++ against include/qrmark and
+    the in-tree libqrmark_b200.so) on `images_np` written to a scratch file."""
+    import subprocess
+    import tempfile
+    src = os.path.join(ROOT, "tests", "cpp", "bench_dropin.cpp")
+    libdir = os.path.join(ROOT, "paper_2509_02447_b200", "_lib")
+    exe = os.path.join(ROOT, "tests", "cpp", "_build", "bench_dropin")
+    deps = [src, os.path.join(libdir, "libqrmark_b200.so"), os.path.join(ROOT, "include", "qrmark", "api.hpp")]
+    if not os.path.exists(exe) or any(os.path.getmtime(d) > os.path.getmtime(exe) for d in deps):
+        os.makedirs(os.path.dirname(exe), exist_ok=True)
+        subprocess.run(["g++", "-std=c++20", "-O2", src, "-I", os.path.join(ROOT, "include"), "-L", libdir,
+                        "-lqrmark_b200", f"-Wl,-rpath,{libdir}", "-o", exe], check=True, capture_output=True)
+    n, h, w, _ = images_np.shape
+    with tempfile.NamedTemporaryFile(suffix=".u8") as f:
+        images_np.tofile(f.name)
+        env = dict(os.environ, CUDA_VISIBLE_DEVICES=str(device))
+        r = subprocess.run([exe, f.name, str(n), str(w), str(h), str(max(5, args.steps // 5)), str(args.warmup)],
+                           capture_output=True, text=True, timeout=300, env=env)
+    if r.returncode != 0:
+        raise RuntimeError(r.stderr[-300:])
+    res = json.loads(r.stdout.strip().splitlines()[-1])
+    return {"value": res["images_per_s"], "unit": "images/s", "h2d_bytes_per_step": n * 3 * 64 * 64,
+            "d2h_bytes_per_step": n * 24, "path": "qrmark::detect_batch(std::vector<ImageBuffer>) (C++ drop-in, "
+            "per-image pageable buffers, staged windows, fresh DetectionContext per call)", **res}
 
 
 def hidden_submetric(ctx, pool, world, max_over_ranks, stream, batch=BATCH, reps=5, host_pool=None):
@@ -286,6 +333,10 @@ def main():
 
     # Corpus pool on the device (cmd_bench recipe); each rank its own images.
     pool = q.make_corpus(cfg, 1000 + rank * POOL, POOL, W, H)
+    torch.cuda.synchronize()
+    # the pool is complete before the timed loop, and only decodes follow on the
+    # stream: each decode's window loads may overlap the previous decode's tail
+    ctx.set_input_overlap(True)
     nb = POOL // BATCH
     out = torch.empty((BATCH, q.RECORD_DTYPE.itemsize), dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream()
@@ -391,6 +442,16 @@ def main():
                      "h2d_bytes_per_step": int(st["h2d_bytes"]), "d2h_bytes_per_step": int(st["d2h_bytes"])}
         assert recs_h["verified"].all()
 
+    # The C++ drop-in (qrmark::detect_batch over a std::vector<ImageBuffer> of
+    # separate pageable images, a fresh DetectionContext per call, CorrectionCache
+    # hit flags) on the same 4096-image batches: tests/cpp/bench_dropin.cpp.
+    e2e_dropin = None
+    if world == 1:
+        try:
+            e2e_dropin = dropin_submetric(host_pool[:BATCH].numpy(), args, local)
+        except Exception as exc:
+            e2e_dropin = {"unavailable": str(exc)[-300:]}
+
     # configs[4]: 1M 256x256 images per job, sharded over the ranks (each rank
     # 1M/world images with its global draw range), host images -> host records
     # in calls of 8,192 (mode 0) over this rank's pinned pool.
@@ -478,6 +539,7 @@ def main():
     # Robustness sweep (the paper's Table 3 analogue): each
     # attack of attack_suite on the device, then detection; TPR and bit accuracy.
     robustness = {}
+    ctx.set_input_overlap(False)  # the attack kernel writes the images just before each decode
     try:
         imgs = pool[:BATCH]
         out_r = torch.empty((BATCH, q.RECORD_DTYPE.itemsize), dtype=torch.uint8, device=dev)
@@ -503,7 +565,7 @@ def main():
         try:
             rates, info = cpu_reference_run(steps=3, warmup=1, sample=int(os.environ.get("QRM_REF_SAMPLE", "8192")))
             cpu = {"value": statistics.median(rates), "unit": "images/s", "cores": info["cores"],
-                   "kind": info["kind"], "sample": info["sample"]}
+                   "kind": info["kind"], "cpu_model": info["cpu_model"], "sample": info["sample"]}
             nthreads = os.cpu_count() or 1
             rs["cpu_reference_codewords_per_s"] = cpu_rs_baseline(cpu_words, nthreads)
             rs["cpu_reference_sample"] = f"1,000,000 stress words, bw_decode on {nthreads} threads"
@@ -517,17 +579,14 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "u8 x s8 -> s32 (tcgen05 kind::i8), GF(2^m) integer RS",
             "data": "synthetic (cmd_bench corpus: synthetic_image + embed_image_grid, generated on device)",
-            "config": {"workload": "configs[1]: 256x256 RGB batch 4096, one 64x64 tile/image (random_grid), "
-                                   "spread-spectrum decoder (60 bits) + gf16-15-12 RS + verify",
-                       "global_batch": BATCH * world, "per_gpu_batch": BATCH, "parallelism": f"dp{world} (shards)",
-                       "l2": "inputs rotate over a 16,384-image pool (3.2 GB; each step a different batch and "
-                             "draw range, 4 x 50 MB of tile windows per rotation > 126 MB L2)",
-                       "e2e_modes": {"mapped_window_zero_copy (mode 0, headline)": e2e[0],
-                                     "staged_window_host_gather (mode 2)": e2e[2],
-                                     "zero_copy_70_plus_staged_30 (mode 3)": e2e[3],
-                                     "full_image_h2d (mode 1)": e2e[1]},
-                       "e2e_plan": {"streams": plan[0], "minibatch": plan[1]}},
+            "config": bench_config(world),
             "e2e": e2e[0],
+            "e2e_modes": {"mapped_window_zero_copy (mode 0, headline)": e2e[0],
+                          "staged_window_host_gather (mode 2)": e2e[2],
+                          "zero_copy_70_plus_staged_30 (mode 3)": e2e[3],
+                          "full_image_h2d (mode 1)": e2e[1]},
+            "e2e_plan": {"streams": plan[0], "minibatch": plan[1]},
+            "e2e_dropin": e2e_dropin,
             "gpu_launches": launches,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                          "frac": achieved / hbm, "traffic": traffic, "kernel": "corr_detect_kernel",

@@ -19,6 +19,8 @@
 #include <cstdint>
 #include <filesystem>
 #include <functional>
+#include <list>
+#include <memory>
 #include <mutex>
 #include <optional>
 #include <span>
@@ -256,9 +258,14 @@ public:
 
 private:
     size_t samples() const { return static_cast<size_t>(tile_size_) * tile_size_ * 3; }
+    const int8_t* planes() const;  // host copy of the device planes, built on first use
+    struct HostPlanes {
+        std::once_flag once;
+        std::vector<int8_t> v;
+    };
     WatermarkKey key_;
     int tile_size_;
-    std::vector<int8_t> patterns_;  // host copy of the device planes (for residual/correlation)
+    std::shared_ptr<HostPlanes> host_planes_ = std::make_shared<HostPlanes>();  // shared by copies (immutable)
 };
 void embed_image_grid(ImageBuffer& normalized_img, const SpreadSpectrumCodec& codec, const BitVec& bits);
 ImageBuffer embed(const ImageBuffer& tile, const BitVec& bits, const WatermarkKey& key);
@@ -373,6 +380,11 @@ public:
     std::pair<std::optional<DecodeResult>, bool> correct(const BitVec& raw, const CodeParams& params);
     // correct()'s bookkeeping for a word decoded elsewhere (the GPU): returns the hit flag.
     bool record(const BitVec& raw, const std::optional<DecodeResult>& decoded);
+    // The same, building the stored result only on a miss.
+    bool record(const BitVec& raw, const std::function<std::optional<DecodeResult>()>& decoded_on_miss);
+    // The same for a packed raw word (n_bits <= 64, bit 0 of the BitVec in the word's top used bit).
+    bool record_packed(uint64_t raw_word, int n_bits,
+                       const std::function<std::optional<DecodeResult>()>& decoded_on_miss);
     size_t size() const;
     uint64_t hits() const { return hits_; }
     uint64_t lookups() const { return lookups_; }
@@ -381,11 +393,16 @@ private:
     struct Entry {
         std::optional<DecodeResult> result;
         uint64_t last_access = 0;
+        std::list<std::string>::iterator pos;  // place in lru_
     };
+    bool record_key(std::string key, const std::function<std::optional<DecodeResult>()>& decoded_on_miss);
+    void touch_locked(Entry& e);
+    void insert_locked(std::string key, std::optional<DecodeResult> result);
     void evict_locked();
     CacheConfig cfg_;
     mutable std::mutex mu_;
     std::unordered_map<std::string, Entry> map_;
+    std::list<std::string> lru_;  // keys, least recently used first
     uint64_t tick_ = 0, hits_ = 0, lookups_ = 0;
 };
 
@@ -402,9 +419,12 @@ public:
     const BitVec& key_codeword() const { return key_codeword_; }
     CorrectionCache& cache() { return cache_; }
     DetectionRecord detect_one(const ImageBuffer& img, uint64_t draw_index);
-    // Batch entry used by detect_batch: records for images with draw_index first_draw + i.
+    // Batch entry used by detect_batch: records for images with draw_index first_draw + i,
+    // with the reference's optional SyntheticStageLoad and DeskReport (detect.cpp:250-368).
     std::vector<DetectionRecord> detect_many(std::span<const ImageBuffer> images, uint64_t first_draw,
-                                             const StreamPlan* plan = nullptr);
+                                             const StreamPlan* plan = nullptr,
+                                             const struct SyntheticStageLoad* load = nullptr,
+                                             struct DeskReport* report = nullptr);
     GpuContext* gpu() { return gpu_; }
 
 private:
@@ -427,7 +447,15 @@ struct DeskReport {
     size_t items = 0;
 };
 // The CUDA-stream pipeline: plan->streams are the per-stage stream counts of
-// the transfer / decode / correct stages, plan->minibatch their mini-batch.
+// the transfer / decode / correct stages (the reference's worker pools), the
+// mini-batch is the largest plan->minibatch entry (the reference's queue batch).
+// Same-size images of >= 256 px move only their l x l windows (host workers
+// gather them into the context's pinned staging ring); other batches take the
+// ragged path. load: each stage's stream is held load_ns per image of every
+// mini-batch it processes (the reference's per-item synthetic_wait); a non-zero
+// load needs the stage pipeline (same-size images >= 256 px), else InvalidInput.
+// report: wall time, per-stage busy time (cudaEvent spans summed over
+// mini-batches) and stream counts; records' stage_ns are their mini-batch's spans.
 std::vector<DetectionRecord> detect_batch(std::span<const ImageBuffer> images, const DetectionConfig& cfg,
                                           const StreamPlan* plan = nullptr, const SyntheticStageLoad* load = nullptr,
                                           DeskReport* report = nullptr);

@@ -4,7 +4,7 @@
  * This is the drop-in boundary: plain C types, plain pointers and sizes, no
  * C++ or torch types. Each entry point names the reference interface it
  * replaces (paths relative to /root/reference/proj). The C++ drop-in API
- * (include/qrmark/*.hpp, namespace qrmark) and the Python package
+ * (include/qrmark/<module>.hpp, namespace qrmark) and the Python package
  * (paper_2509_02447_b200) are both thin layers over these calls.
  *
  * Conventions
@@ -97,6 +97,28 @@ typedef struct qrm_host_stats {
     int kernel_launches;
 } qrm_host_stats;
 
+/* SyntheticStageLoad (detect.hpp:127-131): extra work per image in each
+ * stage (preprocess / extract / correct in the reference; transfer / decode /
+ * correct+return here). The reference sleeps ns per item in each worker
+ * (detect.cpp:243-245, 304, 318, 336); here each mini-batch of b images on a
+ * stage's stream is held for b * ns by a device-side wait on that stream, so
+ * s concurrent streams of a stage model s workers, as in the reference. */
+typedef struct qrm_stage_load {
+    int64_t ns[3];
+} qrm_stage_load;
+
+/* DeskReport / StageLatencies accounting (detect.hpp:39-43, 134-139) of one
+ * host-pipeline call, from cudaEvents on the stage streams (plus the host
+ * gather time of the staged transfer): busy_ns[k] = sum over mini-batches of
+ * stage k's span; image_ns (nullable, caller-owned count x 3) = the stage spans
+ * of each image's mini-batch (every image of a mini-batch is in flight for the
+ * whole span). */
+typedef struct qrm_stage_times {
+    int64_t wall_ns;
+    int64_t busy_ns[3];
+    int64_t* image_ns;
+} qrm_stage_times;
+
 typedef struct qrm_ctx qrm_ctx;
 
 QRM_EXPORT const char* qrm_last_error(void);
@@ -124,6 +146,15 @@ QRM_EXPORT qrm_status qrm_ctx_info(const qrm_ctx* ctx, uint64_t* key_codeword, u
 QRM_EXPORT qrm_status qrm_detect_device(qrm_ctx* ctx, const uint8_t* images, int64_t count, int w, int h,
                                         int64_t image_stride, uint64_t first_draw, qrm_record* out, void* stream);
 
+/* Stream overlap of qrm_detect_device. The decode kernel is launched with
+ * programmatic dependent launch: by default (enable = 0) it reads no window
+ * before the preceding kernel on the stream has completed, so the images may
+ * be produced by any kernel just before the call. enable = 1 is the caller's
+ * promise that the images are complete before the preceding kernel on the
+ * stream runs (e.g. a resident batch decoded back to back): the window loads
+ * then overlap the previous decode's tail. Records are identical either way. */
+QRM_EXPORT qrm_status qrm_ctx_set_input_overlap(qrm_ctx* ctx, int enable);
+
 /* Same, from HOST images to HOST records, through the stream pipeline (the
  * CUDA-stream executor that replaces detect_batch's thread pools and bounded
  * queues). plan == NULL uses the context's current plan (qrm_ctx_set_plan).
@@ -138,6 +169,25 @@ QRM_EXPORT qrm_status qrm_detect_device(qrm_ctx* ctx, const uint8_t* images, int
 QRM_EXPORT qrm_status qrm_detect_host(qrm_ctx* ctx, const uint8_t* images, int64_t count, int w, int h,
                                       int64_t image_stride, uint64_t first_draw, qrm_record* out,
                                       const qrm_plan* plan, int mode, qrm_host_stats* stats);
+
+/* qrm_detect_host with the reference's SyntheticStageLoad and DeskReport stage
+ * accounting (both nullable). */
+QRM_EXPORT qrm_status qrm_detect_host_timed(qrm_ctx* ctx, const uint8_t* images, int64_t count, int w, int h,
+                                            int64_t image_stride, uint64_t first_draw, qrm_record* out,
+                                            const qrm_plan* plan, int mode, const qrm_stage_load* load,
+                                            qrm_stage_times* times);
+
+/* detect_batch over a std::span<const ImageBuffer> (detect.cpp:250-368): `count`
+ * same-size w x h images at separate, pageable host addresses images[i] (each
+ * ImageBuffer's own bytes; nothing is registered or copied whole). The staged
+ * transfer (mode 2) moves only each image's l x l window: the context's host
+ * workers gather the windows into a context-owned pinned staging ring that the
+ * copy engine moves to the device while the next piece is gathered. Needs
+ * min(w, h) >= 256 (inputs that need the bilinear upscale take
+ * qrm_detect_ragged). load / times as qrm_detect_host_timed. */
+QRM_EXPORT qrm_status qrm_detect_host_images(qrm_ctx* ctx, const uint8_t* const* images, int64_t count, int w,
+                                             int h, uint64_t first_draw, qrm_record* out, const qrm_plan* plan,
+                                             const qrm_stage_load* load, qrm_stage_times* times);
 
 /* Ragged batch (std::span<const ImageBuffer> of mixed sizes, detect.hpp:145):
  * per-image host pointers and sizes. Images smaller than 256 px take the
@@ -192,6 +242,15 @@ QRM_EXPORT qrm_status qrm_detect_host_multi(qrm_ctx* const* ctxs, int nctx, cons
 QRM_EXPORT qrm_status qrm_extract_tiles_device(qrm_ctx* ctx, const uint8_t* images, int64_t count, int w, int h,
                                                int64_t image_stride, uint64_t first_draw, int channels, void* out,
                                                void* stream);
+
+/* Diagnostics for the learned extractor's per-layer checks
+ * (scripts/debug_hidden_layers.py): runs conv layers 0..stop_after on a device
+ * batch and copies that layer's output to `out` -- bf16 NHWC
+ * [count][64][64][64] activations, or for the last layer (stop_after = 8) the
+ * fp32 per-block channel sums [count][32][64]. */
+QRM_EXPORT qrm_status qrm_hidden_debug_activation(qrm_ctx* ctx, const uint8_t* images, int64_t count, int w, int h,
+                                                  int64_t image_stride, uint64_t first_draw, uint64_t weight_seed,
+                                                  int stop_after, void* out, void* stream);
 
 /* Extractor behind the WatermarkCodec plug-in point (stego.hpp:32-40) used by
  * qrm_detect_device / qrm_detect_host / qrm_detect_ragged:

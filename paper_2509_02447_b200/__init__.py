@@ -33,6 +33,7 @@ ABI_SYMBOLS = (
     "qrm_verify_threshold", "qrm_make_corpus_device", "qrm_patterns_device", "qrm_allocate_streams",
     "qrm_lpt_schedule", "qrm_warmup_profile", "qrm_ctx_set_plan", "qrm_kernel_launch_count",
     "qrm_probe_decode_kernel", "qrm_resample_host", "qrm_extract_float_host", "qrm_hidden_detect_device",
+    "qrm_ctx_set_input_overlap", "qrm_hidden_debug_activation", "qrm_detect_host_timed", "qrm_detect_host_images",
 )
 
 
@@ -76,6 +77,14 @@ class _Plan(C.Structure):
     _fields_ = [("streams", C.c_int * 3), ("minibatch", C.c_int * 3)]
 
 
+class _StageLoad(C.Structure):
+    _fields_ = [("ns", C.c_int64 * 3)]
+
+
+class _StageTimes(C.Structure):
+    _fields_ = [("wall_ns", C.c_int64), ("busy_ns", C.c_int64 * 3), ("image_ns", C.c_void_p)]
+
+
 class _HostStats(C.Structure):
     _fields_ = [("wall_ms", C.c_double), ("h2d_bytes", C.c_double), ("d2h_bytes", C.c_double),
                 ("minibatches", C.c_int), ("kernel_launches", C.c_int)]
@@ -99,6 +108,12 @@ def lib() -> C.CDLL:
         L.qrm_ctx_info.argtypes = [vp, C.POINTER(u64), C.POINTER(u64), C.POINTER(i32), C.POINTER(i32)]
         L.qrm_ctx_set_extractor.argtypes = [vp, i32, u64]
         L.qrm_ctx_set_transfer_split.argtypes = [vp, C.c_double]
+        L.qrm_ctx_set_input_overlap.argtypes = [vp, i32]
+        L.qrm_detect_host_timed.argtypes = [vp, vp, i64, i32, i32, i64, u64, vp, C.POINTER(_Plan), i32,
+                                            C.POINTER(_StageLoad), C.POINTER(_StageTimes)]
+        L.qrm_detect_host_images.argtypes = [vp, C.POINTER(vp), i64, i32, i32, u64, vp, C.POINTER(_Plan),
+                                             C.POINTER(_StageLoad), C.POINTER(_StageTimes)]
+        L.qrm_hidden_debug_activation.argtypes = [vp, vp, i64, i32, i32, i64, u64, u64, i32, vp, vp]
         L.qrm_detect_host_lpt.argtypes = [vp, vp, i64, i32, i32, i64, u64, vp, C.POINTER(_Plan), i32, C.c_double, i32,
                                           C.POINTER(_HostStats)]
         L.qrm_detect_host_multi.argtypes = [C.POINTER(vp), i32, vp, i64, i32, i32, i64, u64, vp, C.POINTER(_Plan), i32,
@@ -400,6 +415,41 @@ def preprocess(img: np.ndarray) -> np.ndarray:
     return out
 
 
+_U8 = None  # torch.uint8, bound on first use (torch is imported lazily)
+
+
+def _device_images(images, device: int):
+    """Check a device image batch before its address crosses the C-ABI: uint8
+    CUDA tensor [B, H, W, 3] on the context's GPU whose rows and pixels are
+    contiguous (any batch stride). Other layouts are made contiguous; a CPU
+    tensor or one on another GPU is an error (no silent fallback). The common
+    case costs ~1 us (bench.py's back-to-back loop is sensitive to host time)."""
+    global _U8
+    if _U8 is None:
+        import torch
+        _U8 = torch.uint8
+    try:
+        ok = images.dtype == _U8 and images.is_cuda and images.get_device() == device and images.dim() == 4
+    except AttributeError:
+        raise InvalidInput("images must be a CUDA torch.Tensor") from None
+    if not ok:
+        if images.dtype != _U8:
+            raise InvalidInput(f"images must be uint8, got {images.dtype}")
+        if not images.is_cuda:
+            raise InvalidInput("images must be on a CUDA device (use detect_host for host images)")
+        if images.get_device() != device:
+            raise InvalidInput(f"images are on cuda:{images.get_device()}, the context on cuda:{device}")
+        raise InvalidInput(f"images must be [B, H, W, 3] (interleaved RGB), got {tuple(images.shape)}")
+    if images.shape[3] != 3:
+        raise InvalidInput(f"images must be [B, H, W, 3] (interleaved RGB), got {tuple(images.shape)}")
+    if not images.is_contiguous():
+        B, H, W, _ = images.shape
+        st = images.stride()
+        if B > 0 and (st[3] != 1 or st[2] != 3 or st[1] != 3 * W or (B > 1 and st[0] < H * W * 3)):
+            images = images.contiguous()
+    return images
+
+
 class DetectionContext:
     """DetectionContext (detect.hpp:101-119): codec patterns, key codeword, thresholds on one GPU."""
 
@@ -425,6 +475,7 @@ class DetectionContext:
 
     def kernel_time_probe(self, images, reps: int = 20) -> float:
         """Mean duration (ms) of the decode kernel alone on a device batch."""
+        images = _device_images(images, self.device)
         B, H, W, _ = images.shape
         ms = C.c_double()
         _check(lib().qrm_probe_decode_kernel(self._h, _ptr(images), B, W, H, images.stride(0), reps, C.byref(ms)))
@@ -449,6 +500,7 @@ class DetectionContext:
 
     def detect_device(self, images, first_draw: int = 0, out=None, stream=None):
         """Device-resident batch: images uint8 CUDA tensor [B, H, W, 3] -> record tensor [B, 24] (uint8)."""
+        images = _device_images(images, self.device)
         B, H, W, _ = images.shape
         if out is None:
             import torch
@@ -463,6 +515,7 @@ class DetectionContext:
 
         -> (logits float32 [B, N] or None, record tensor [B, 24] uint8)."""
         import torch
+        images = _device_images(images, self.device)
         B, H, W, _ = images.shape
         nb = self.cfg.code.codeword_bits()
         lg = torch.empty((B, nb), dtype=torch.float32, device=images.device) if logits else None
@@ -476,6 +529,7 @@ class DetectionContext:
         """preprocess -> select_tile -> extract_tile -> normalize as bf16 NHWC tiles
         [B, l, l, channels] on the device (channels 4: zero-padded)."""
         import torch
+        images = _device_images(images, self.device)
         B, H, W, _ = images.shape
         l = self.cfg.tile_size
         if out is None:
@@ -486,6 +540,7 @@ class DetectionContext:
 
     def extract_device(self, images, first_draw: int = 0, soft: bool = True, stream=None):
         """SpreadSpectrumCodec::extract + harden on a device batch -> (soft float64 [B, N] or None, raw int64 [B])."""
+        images = _device_images(images, self.device)
         import torch
         B, H, W, _ = images.shape
         nb = self.cfg.code.codeword_bits()
@@ -528,6 +583,45 @@ class DetectionContext:
         return out, {"wall_ms": st.wall_ms, "h2d_bytes": st.h2d_bytes, "d2h_bytes": st.d2h_bytes,
                      "minibatches": st.minibatches, "kernel_launches": st.kernel_launches}
 
+    def detect_images(self, images, first_draw: int = 0, plan=None, load=None, image_ns: bool = False):
+        """detect_batch over separate same-size host images (a list of HxWx3 uint8
+        arrays, >= 256 px): only each image's window is gathered into the context's
+        pinned staging ring and copied. ``load``: SyntheticStageLoad ns per image
+        (transfer, decode, correct). Returns (records, {"wall_ns", "busy_ns",
+        "image_ns" [B, 3] when asked})."""
+        keep = [np.ascontiguousarray(im, dtype=np.uint8) for im in images]
+        n = len(keep)
+        if n == 0:
+            return np.zeros(0, dtype=RECORD_DTYPE), {"wall_ns": 0, "busy_ns": [0, 0, 0]}
+        H, W = keep[0].shape[:2]
+        ptrs = (C.c_void_p * n)(*[a.ctypes.data for a in keep])
+        out = np.zeros(n, dtype=RECORD_DTYPE)
+        pl = _Plan((C.c_int * 3)(*plan[0]), (C.c_int * 3)(*plan[1])) if plan is not None else None
+        ld = _StageLoad((C.c_int64 * 3)(*(load or (0, 0, 0))))
+        ins = np.zeros((n, 3), np.int64) if image_ns else None
+        tm = _StageTimes(0, (C.c_int64 * 3)(0, 0, 0), ins.ctypes.data if ins is not None else None)
+        _check(lib().qrm_detect_host_images(self._h, ptrs, n, W, H, first_draw, out.ctypes.data,
+                                            C.byref(pl) if pl is not None else None, C.byref(ld), C.byref(tm)))
+        info = {"wall_ns": tm.wall_ns, "busy_ns": list(tm.busy_ns)}
+        if ins is not None:
+            info["image_ns"] = ins
+        return out, info
+
+    def detect_host_timed(self, images: np.ndarray, first_draw: int = 0, plan=None, mode: int = 0, load=None):
+        """qrm_detect_host with SyntheticStageLoad and DeskReport-style stage spans
+        -> (records, {"wall_ns", "busy_ns", "image_ns" [B, 3]})."""
+        images = np.ascontiguousarray(images, dtype=np.uint8)
+        B, H, W, _ = images.shape
+        out = np.zeros(B, dtype=RECORD_DTYPE)
+        pl = _Plan((C.c_int * 3)(*plan[0]), (C.c_int * 3)(*plan[1])) if plan is not None else None
+        ld = _StageLoad((C.c_int64 * 3)(*(load or (0, 0, 0))))
+        ins = np.zeros((B, 3), np.int64)
+        tm = _StageTimes(0, (C.c_int64 * 3)(0, 0, 0), ins.ctypes.data)
+        _check(lib().qrm_detect_host_timed(self._h, images.ctypes.data, B, W, H, H * W * 3, first_draw,
+                                           out.ctypes.data, C.byref(pl) if pl is not None else None, mode,
+                                           C.byref(ld), C.byref(tm)))
+        return out, {"wall_ns": tm.wall_ns, "busy_ns": list(tm.busy_ns), "image_ns": ins}
+
     def detect_ragged(self, images, first_draw: int = 0) -> np.ndarray:
         """Mixed-size host images (list of HxWx3 uint8) -> records."""
         keep = [np.ascontiguousarray(im, dtype=np.uint8) for im in images]
@@ -538,6 +632,12 @@ class DetectionContext:
         out = np.zeros(n, dtype=RECORD_DTYPE)
         _check(lib().qrm_detect_ragged(self._h, ptrs, ws, hs, n, first_draw, out.ctypes.data))
         return out
+
+    def set_input_overlap(self, enable: bool):
+        """qrm_ctx_set_input_overlap: promise that detect_device's images are complete
+        before the preceding kernel on the stream (resident batches decoded back to
+        back), letting each decode's window loads overlap the previous decode."""
+        _check(lib().qrm_ctx_set_input_overlap(self._h, int(bool(enable))))
 
     def set_transfer_split(self, zero_copy_fraction: float):
         """Host pipeline mode 3: share of each mini-batch's windows fetched zero-copy."""
@@ -589,10 +689,15 @@ def records_from_device(t) -> np.ndarray:
 def detect_batch(images, cfg: DetectionConfig, plan=None, first_draw: int = 0, device: int = 0, mode: int = 0):
     """detect_batch (detect.cpp:250): list/array of host images -> records (structured array).
 
-    Uniform uint8 arrays go through the stream executor; mixed sizes through the ragged path."""
+    A uniform uint8 array goes through the stream executor (``mode``); a list of
+    same-size images of >= 256 px through the per-image staged path; mixed sizes
+    through the ragged path."""
     with DetectionContext(cfg, device) as ctx:
         if isinstance(images, np.ndarray) and images.ndim == 4:
             return ctx.detect_host(images, first_draw, plan=plan, mode=mode)[0]
+        images = list(images)
+        if images and all(np.shape(im) == np.shape(images[0]) for im in images) and min(np.shape(images[0])[:2]) >= 256:
+            return ctx.detect_images(images, first_draw, plan=plan)[0]
         return ctx.detect_ragged(images, first_draw)
 
 

@@ -59,6 +59,7 @@ cudaError_t launch_build_patterns(uint64_t seed, int nbits, int K, int K_pad, in
 cudaError_t launch_residual(uint64_t seed, int nbits, int K, uint64_t codeword, float* delta, cudaStream_t st);
 cudaError_t launch_extract_float(uint64_t seed, int nbits, int K, const float* tile, double* soft, cudaStream_t st);
 cudaError_t launch_resample(const GatherDesc& d, int out_w, int out_h, int normalize, void* out, cudaStream_t st);
+cudaError_t launch_stage_load(long long ns, cudaStream_t st);
 cudaError_t launch_corpus(uint64_t first_seed, int64_t count, int w, int h, int l, int embed, float alpha,
                           const float* delta, uint8_t* out, cudaStream_t st);
 }  // namespace qrm
@@ -161,10 +162,8 @@ struct Workspace {
     int64_t images_cap = 0;
     uint8_t* host_stage = nullptr;  // pinned window staging (host pipeline, mode 2)
     int64_t host_stage_cap = 0;
-    cudaEvent_t host_stage_free = nullptr;  // H2D out of host_stage finished
     void release() {
         if (host_stage) cudaFreeHost(host_stage);
-        if (host_stage_free) cudaEventDestroy(host_stage_free);
         cudaFree(pending_count);
         cudaFree(pending);
         cudaFree(stage);
@@ -195,10 +194,18 @@ struct qrm_ctx {
     std::unique_ptr<HostPool> pool;  // window staging workers (host pipeline, modes 2 and 3)
     cudaStream_t copy_stream = nullptr;  // mode 3: copy-engine H2D of the staged windows
     std::vector<cudaEvent_t> events;     // host pipeline events, reused call to call
+    std::vector<cudaEvent_t> timing_events;  // the same with timing, for calls that report stage spans
     double hybrid_fraction = 0.5;        // mode 3: share of each mini-batch fetched zero-copy
     int64_t stage_piece = 512;           // modes 2/3: windows gathered per H2D
     double decode_ms_per_image = 0.0;  // from the last warm-up profile (Algorithm 2 latencies)
     int extractor = QRM_EXTRACTOR_SPREAD_SPECTRUM;  // qrm_ctx_set_extractor
+    bool input_overlap = false;  // qrm_ctx_set_input_overlap
+    qrm_record* host_records = nullptr;  // pinned D2H target when the caller's record buffer is pageable
+    int64_t host_records_cap = 0;
+    // A/B switches, read once at context creation
+    int corr_ksplit = 0;            // QRM_CORR_KSPLIT: forced split-K cluster size (0: automatic)
+    bool conv_pair = true;          // QRM_CONV_PAIR=0: single-CTA conv layer
+    bool conv_fuse_linear = true;   // QRM_CONV_FUSE_LINEAR=0: unfused head
     uint64_t conv_seed = 7;
     // learned (conv) extractor: folded weights + activation ping-pong buffers
     struct Hidden {
@@ -273,75 +280,41 @@ qrm_status hidden_run(qrm_ctx* c, Workspace& W, const WindowSource& src, int64_t
 // Decode + correct `count` windows described by src into device records.
 cudaEvent_t g_probe[2] = {nullptr, nullptr};  // set only by qrm_probe_decode_kernel
 
+// wait_inputs: the windows may come from the kernel launched just before on
+// `st` (gather, corpus, caller kernels), so the decode must not read them
+// before griddepcontrol.wait. Only callers that know the preceding work on `st`
+// is complete by stream-event order (the host executor) or is another decode
+// (qrm_ctx_set_input_overlap) pass false.
 qrm_status run_detect(qrm_ctx* c, Workspace& w, const WindowSource& src, int64_t count, qrm_record* out,
                       double* soft, uint64_t* raw, cudaStream_t st, cudaEvent_t mid_event = nullptr,
-                      cudaStream_t finish_stream = nullptr) {
+                      cudaStream_t finish_stream = nullptr, bool wait_inputs = true, long long load_ns = 0,
+                      cudaEvent_t finish_start = nullptr) {
     qrm_status s = workspace_reserve(w, count);
     if (s != QRM_OK) return s;
     if (c->extractor == QRM_EXTRACTOR_CONV) {
         // learned extractor: conv stack + head (+ RS finish) on st
         if ((s = hidden_run(c, w, src, count, out, nullptr, st)) != QRM_OK) return s;
+        if (load_ns > 0) QRM_LAUNCH(launch_stage_load(load_ns, st));
         if (mid_event && finish_stream) {
             QRM_CUDA(cudaEventRecord(mid_event, st));
             QRM_CUDA(cudaStreamWaitEvent(finish_stream, mid_event, 0));
+            if (finish_start) QRM_CUDA(cudaEventRecord(finish_start, finish_stream));
         }
         return QRM_OK;
     }
     DetectParams p = base_params(c, w, count, out, soft, raw);
     p.src = src;
     if (g_probe[0]) QRM_CUDA(cudaEventRecord(g_probe[0], st));
-    std::vector<unsigned long long> dbg;
-    unsigned long long* d_dbg = nullptr;
-    const int64_t max_ctas = ((count + 15) / 16) * 4 + 8;
-    if (getenv("QRM_DEBUG_TIMES")) {  // diagnostics: per-CTA phase timeline of the decode kernel
-        QRM_CUDA(cudaMalloc(&d_dbg, sizeof(unsigned long long) * 8 * max_ctas));
-        QRM_CUDA(cudaMemsetAsync(d_dbg, 0, sizeof(unsigned long long) * 8 * max_ctas, st));
-        p.dbg_times = d_dbg;
-    }
-    long long* d_stg = nullptr;
-    if (getenv("QRM_DEBUG_STAGES")) {  // diagnostics: per-stage issue / arrival clocks of CTAs 0-7
-        QRM_CUDA(cudaMalloc(&d_stg, sizeof(long long) * 8 * 256));
-        QRM_CUDA(cudaMemsetAsync(d_stg, 0, sizeof(long long) * 8 * 256, st));
-        p.dbg_stages = d_stg;
-    }
+    p.wait_inputs = wait_inputs ? 1 : 0;
+    p.ksplit = c->corr_ksplit;
     QRM_LAUNCH(launch_corr_detect(p, c->sms, st));
-    if (d_stg) {
-        std::vector<long long> h(8 * 256);
-        QRM_CUDA(cudaMemcpyAsync(h.data(), d_stg, sizeof(long long) * h.size(), cudaMemcpyDeviceToHost, st));
-        QRM_CUDA(cudaStreamSynchronize(st));
-        cudaFree(d_stg);
-        for (int b = 0; b < 2; ++b) {
-            const long long t0 = h[b * 256];
-            fprintf(stderr, "[qrm stages] count=%lld cta %d issue:", static_cast<long long>(count), b);
-            for (int i = 0; i < 128 && h[b * 256 + i]; ++i) fprintf(stderr, " %lld", h[b * 256 + i] - t0);
-            fprintf(stderr, "\n[qrm stages] count=%lld cta %d full: ", static_cast<long long>(count), b);
-            for (int i = 0; i < 128 && h[b * 256 + 128 + i]; ++i) fprintf(stderr, " %lld", h[b * 256 + 128 + i] - t0);
-            fprintf(stderr, "\n");
-        }
-    }
-    if (d_dbg) {
-        dbg.resize(8 * max_ctas);
-        QRM_CUDA(cudaMemcpyAsync(dbg.data(), d_dbg, sizeof(unsigned long long) * dbg.size(), cudaMemcpyDeviceToHost, st));
-        QRM_CUDA(cudaStreamSynchronize(st));
-        cudaFree(d_dbg);
-        unsigned long long t0 = ~0ull;
-        for (int64_t i = 0; i < max_ctas; ++i)
-            if (dbg[i * 8]) t0 = std::min(t0, dbg[i * 8]);
-        for (int ph = 0; ph < 8; ++ph) {
-            std::vector<double> v;
-            for (int64_t i = 0; i < max_ctas; ++i)
-                if (dbg[i * 8 + ph]) v.push_back(static_cast<double>(dbg[i * 8 + ph] - t0) / 1e3);
-            std::sort(v.begin(), v.end());
-            if (!v.empty())
-                fprintf(stderr, "[qrm dbg] count=%lld phase %d: n=%zu min %.2f med %.2f max %.2f us\n",
-                        static_cast<long long>(count), ph, v.size(), v.front(), v[v.size() / 2], v.back());
-        }
-    }
     if (g_probe[1]) QRM_CUDA(cudaEventRecord(g_probe[1], st));
+    if (load_ns > 0) QRM_LAUNCH(launch_stage_load(load_ns, st));  // SyntheticStageLoad of the decode stage
     cudaStream_t fs = st;
     if (mid_event && finish_stream) {
         QRM_CUDA(cudaEventRecord(mid_event, st));
         QRM_CUDA(cudaStreamWaitEvent(finish_stream, mid_event, 0));
+        if (finish_start) QRM_CUDA(cudaEventRecord(finish_start, finish_stream));
         fs = finish_stream;
     }
     // t = 1 codes leave nothing pending (the decode kernel resolves its own ties)
@@ -404,12 +377,15 @@ qrm_status window_source(qrm_ctx* c, Workspace& w, const uint8_t* images, int64_
 
 qrm_status detect_uniform(qrm_ctx* c, Workspace& w, const uint8_t* images, int64_t count, int width, int height,
                           int64_t stride, uint64_t first_draw, qrm_record* out, double* soft, uint64_t* raw,
-                          cudaStream_t st, cudaEvent_t mid = nullptr, cudaStream_t fs = nullptr) {
+                          cudaStream_t st, cudaEvent_t mid = nullptr, cudaStream_t fs = nullptr,
+                          bool overlap_ok = false, long long load_ns = 0, cudaEvent_t finish_start = nullptr) {
     if (count == 0) return QRM_OK;
     WindowSource src;
     const qrm_status s = window_source(c, w, images, count, width, height, stride, first_draw, st, src);
     if (s != QRM_OK) return s;
-    return run_detect(c, w, src, count, out, soft, raw, st, mid, fs);
+    // staged windows come from the gather kernel just launched on st
+    return run_detect(c, w, src, count, out, soft, raw, st, mid, fs, !(overlap_ok && src.direct), load_ns,
+                      finish_start);
 }
 
 qrm_status check_uniform(const qrm_ctx* c, const uint8_t* images, int64_t count, int w, int h, int64_t stride) {
@@ -489,10 +465,10 @@ QRM_EXPORT qrm_status qrm_ctx_create(int device, const qrm_config* cfg, qrm_ctx*
     c->K = 3 * c->l * c->l;
     c->K_pad = (c->K + 127) / 128 * 128;
     QRM_CUDA(cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, device));
-    if (const char* g = getenv("QRM_L2_FETCH")) {  // experiment hook: max L2 fetch granularity (bytes)
-        cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, static_cast<size_t>(atoi(g)));
-        cudaGetLastError();
-    }
+    if (const char* e = getenv("QRM_CORR_KSPLIT")) c->corr_ksplit = atoi(e);
+    if (const char* e = getenv("QRM_CONV_PAIR")) c->conv_pair = e[0] != '0';
+    if (const char* e = getenv("QRM_CONV_FUSE_LINEAR")) c->conv_fuse_linear = e[0] != '0';
+    if (const char* e = getenv("QRM_STAGE_PIECE")) c->stage_piece = std::max<int64_t>(16, atoll(e));
     for (int i = 0; i < kbits; ++i) c->key_msg = (c->key_msg << 1) | (c->key_message[i] & 1);
     c->key_cw = encode_packed(c->m, c->n, c->k, c->key_msg);
     c->tau_msg = verify_threshold(kbits, cfg->fpr_target);
@@ -514,6 +490,8 @@ QRM_EXPORT void qrm_ctx_destroy(qrm_ctx* c) {
     for (auto s : c->streams) cudaStreamDestroy(s);
     if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
     for (auto e : c->events) cudaEventDestroy(e);
+    for (auto e : c->timing_events) cudaEventDestroy(e);
+    if (c->host_records) cudaFreeHost(c->host_records);
     cudaFree(c->d_patterns);
     cudaFree(c->d_colsum);
     cudaFree(c->d_records);
@@ -553,7 +531,13 @@ QRM_EXPORT qrm_status qrm_detect_device(qrm_ctx* c, const uint8_t* images, int64
     if (count > 0 && !out) return fail(QRM_INVALID_INPUT, "null record buffer");
     if ((s = set_device(c->device)) != QRM_OK) return s;
     return detect_uniform(c, c->ws[0], images, count, w, h, stride, first_draw, out, nullptr, nullptr,
-                          as_stream(stream));
+                          as_stream(stream), nullptr, nullptr, c->input_overlap);
+}
+
+QRM_EXPORT qrm_status qrm_ctx_set_input_overlap(qrm_ctx* c, int enable) {
+    if (!c) return fail(QRM_INVALID_INPUT, "null context");
+    c->input_overlap = enable != 0;
+    return QRM_OK;
 }
 
 QRM_EXPORT qrm_status qrm_probe_decode_kernel(qrm_ctx* c, const uint8_t* images, int64_t count, int w, int h,
@@ -568,7 +552,7 @@ QRM_EXPORT qrm_status qrm_probe_decode_kernel(qrm_ctx* c, const uint8_t* images,
     double total = 0.0;
     for (int i = 0; i < reps && s == QRM_OK; ++i) {
         s = detect_uniform(c, c->ws[0], images, count, w, h, stride, static_cast<uint64_t>(i) * count, c->d_records,
-                           nullptr, nullptr, nullptr);
+                           nullptr, nullptr, nullptr, nullptr, nullptr, true);  // resident images, decodes only
         cudaEventSynchronize(g_probe[1]);
         float ms = 0.f;
         cudaEventElapsedTime(&ms, g_probe[0], g_probe[1]);
@@ -688,11 +672,28 @@ struct HostPiece {
     int stream;
 };
 
+// Optional parts of a host-pipeline call.
+struct HostCallOpts {
+    const uint8_t* const* ptrs = nullptr;  // per-image host addresses (qrm_detect_host_images): staged transfer
+    const qrm_stage_load* load = nullptr;  // SyntheticStageLoad
+    qrm_stage_times* times = nullptr;      // DeskReport / StageLatencies accounting
+};
+
 qrm_status detect_host_impl(qrm_ctx* c, const uint8_t* images, int64_t count, int w, int h, int64_t stride,
                             uint64_t first_draw, qrm_record* out, const qrm_plan* plan, int mode,
-                            qrm_host_stats* stats, const std::vector<HostPiece>* pieces) {
-    qrm_status s = check_uniform(c, images, count, w, h, stride);
-    if (s != QRM_OK) return s;
+                            qrm_host_stats* stats, const std::vector<HostPiece>* pieces,
+                            const HostCallOpts& opt = HostCallOpts{}) {
+    qrm_status s;
+    if (opt.ptrs) {
+        if (!c) return fail(QRM_INVALID_INPUT, "null context");
+        if (count < 0) return fail(QRM_INVALID_INPUT, "negative image count");
+        if (w <= 0 || h <= 0) return fail(QRM_INVALID_INPUT, "image dimensions must be positive");
+        for (int64_t i = 0; i < count; ++i)
+            if (!opt.ptrs[i]) return fail(QRM_INVALID_INPUT, "null image pointer");
+        mode = 2;  // separate pageable images: only their windows are staged and copied
+    } else if ((s = check_uniform(c, images, count, w, h, stride)) != QRM_OK) {
+        return s;
+    }
     if (count > 0 && !out) return fail(QRM_INVALID_INPUT, "null record buffer");
     if (mode < 0 || mode > 3)
         return fail(QRM_INVALID_INPUT,
@@ -701,11 +702,26 @@ qrm_status detect_host_impl(qrm_ctx* c, const uint8_t* images, int64_t count, in
     const qrm_plan P = plan ? *plan : c->plan;
     for (int k = 0; k < 3; ++k)
         if (P.streams[k] < 1 || P.minibatch[k] < 1) return fail(QRM_INVALID_INPUT, "plan has an empty stage");
+    long long load_ns[3] = {0, 0, 0};
+    if (opt.load)
+        for (int k = 0; k < 3; ++k) {
+            if (opt.load->ns[k] < 0) return fail(QRM_INVALID_INPUT, "synthetic stage load must be >= 0");
+            load_ns[k] = opt.load->ns[k];
+        }
     const int64_t t0 = now_ns();
+    if (opt.times) {
+        opt.times->wall_ns = 0;
+        for (int k = 0; k < 3; ++k) opt.times->busy_ns[k] = 0;
+    }
     if (count == 0) return QRM_OK;
+    const int64_t img_bytes = static_cast<int64_t>(w) * h * 3;
+    int up, sw, sh, xo, yo;
+    geometry(w, h, up, sw, sh, xo, yo);
+    if (opt.ptrs && up) return fail(QRM_INVALID_INPUT, "per-image host batches need min(w, h) >= 256 (use the ragged path)");
+    auto image_at = [&](int64_t i) -> const uint8_t* { return opt.ptrs ? opt.ptrs[i] : images + i * stride; };
 
     // Host buffers must be page-locked and mapped; register them for the call if not.
-    const int64_t in_bytes = (count - 1) * stride + static_cast<int64_t>(w) * h * 3;
+    const int64_t in_bytes = opt.ptrs ? 0 : (count - 1) * stride + img_bytes;
     bool reg_in = false, reg_out = false;
     int nstreams_used = 0;
     // Every exit path (errors included) drains the streams this call used
@@ -717,19 +733,31 @@ qrm_status detect_host_impl(qrm_ctx* c, const uint8_t* images, int64_t count, in
         if (reg_out) cudaHostUnregister(out);
     });
     cudaPointerAttributes attr{};
-    if (cudaPointerGetAttributes(&attr, images) != cudaSuccess || attr.type != cudaMemoryTypeHost) {
-        cudaGetLastError();
-        QRM_CUDA(cudaHostRegister(const_cast<uint8_t*>(images), in_bytes,
-                                  cudaHostRegisterMapped | cudaHostRegisterReadOnly));
-        reg_in = true;
+    uint8_t* dimg = nullptr;
+    if (!opt.ptrs) {
+        if (cudaPointerGetAttributes(&attr, images) != cudaSuccess || attr.type != cudaMemoryTypeHost) {
+            cudaGetLastError();
+            QRM_CUDA(cudaHostRegister(const_cast<uint8_t*>(images), in_bytes,
+                                      cudaHostRegisterMapped | cudaHostRegisterReadOnly));
+            reg_in = true;
+        }
+        QRM_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&dimg), const_cast<uint8_t*>(images), 0));
     }
+    // Records go D2H into pinned memory: the caller's buffer when it is pinned,
+    // else the context's pinned record buffer (copied out at the end; cheaper
+    // than registering the caller's buffer every call).
+    qrm_record* hout = out;
     if (cudaPointerGetAttributes(&attr, out) != cudaSuccess || attr.type != cudaMemoryTypeHost) {
         cudaGetLastError();
-        QRM_CUDA(cudaHostRegister(out, sizeof(qrm_record) * count, cudaHostRegisterDefault));
-        reg_out = true;
+        if (c->host_records_cap < count) {
+            if (c->host_records) cudaFreeHost(c->host_records);
+            c->host_records = nullptr;
+            c->host_records_cap = 0;
+            QRM_CUDA(cudaHostAlloc(&c->host_records, sizeof(qrm_record) * count, cudaHostAllocDefault));
+            c->host_records_cap = count;
+        }
+        hout = c->host_records;
     }
-    uint8_t* dimg = nullptr;
-    QRM_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&dimg), const_cast<uint8_t*>(images), 0));
 
     // Streams: [0, s0) transfer, [s0, s0+s1) decode, [s0+s1, s0+s1+s2) correct/return.
     const int s0 = P.streams[0], s1 = P.streams[1], s2 = P.streams[2];
@@ -745,9 +773,6 @@ qrm_status detect_host_impl(qrm_ctx* c, const uint8_t* images, int64_t count, in
     if (static_cast<int>(c->ws.size()) < 1 + s1) c->ws.resize(1 + s1);
     if ((s = ensure(c->d_records, c->records_cap, count)) != QRM_OK) return s;
     // Full-image mode: one device image buffer per decode slot.
-    const int64_t img_bytes = static_cast<int64_t>(w) * h * 3;
-    int up, sw, sh, xo, yo;
-    geometry(w, h, up, sw, sh, xo, yo);
     if ((mode == 2 || mode == 3) && up) mode = 1;  // upscaled inputs need the device bilinear gather
     if (mode == 3 && !(direct_ok(c, dimg, w, h, stride) && (3 * c->l) % 16 == 0)) mode = 2;
     if (mode == 1)
@@ -762,27 +787,32 @@ qrm_status detect_host_impl(qrm_ctx* c, const uint8_t* images, int64_t count, in
         for (int j = 0; j < s1; ++j) {
             Workspace& W = c->ws[1 + j];
             if ((s = ensure(W.stage, W.stage_cap, mb * c->K)) != QRM_OK) return s;
-            if (W.host_stage_cap < mb * c->K) {
+            if (W.host_stage_cap < mb * c->K) {  // the context's pinned staging ring, reused call to call
                 if (W.host_stage) cudaFreeHost(W.host_stage);
                 W.host_stage = nullptr;
+                W.host_stage_cap = 0;
                 QRM_CUDA(cudaHostAlloc(&W.host_stage, mb * c->K, cudaHostAllocDefault));
                 W.host_stage_cap = mb * c->K;
             }
-            if (!W.host_stage_free) QRM_CUDA(cudaEventCreateWithFlags(&W.host_stage_free, cudaEventDisableTiming));
         }
     }
 
     nstreams_used = nstreams;
     const int64_t nwork = pieces ? static_cast<int64_t>(pieces->size()) : nmb;
-    // events come from the context's pool (creating ~20 per call cost ~50 us)
-    const size_t nev = static_cast<size_t>(4 * nstreams + 4 * nwork);
-    while (c->events.size() < nev) {
+    // events come from the context's pools (creating ~20 per call cost ~50 us);
+    // timing-enabled ones only when the call asks for stage accounting
+    const bool timed = opt.times != nullptr;
+    std::vector<cudaEvent_t>& pool_ev = timed ? c->timing_events : c->events;
+    const size_t nev = static_cast<size_t>(4 * nstreams + 8 * nwork);
+    while (pool_ev.size() < nev) {
         cudaEvent_t e;
-        QRM_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-        c->events.push_back(e);
+        QRM_CUDA(cudaEventCreateWithFlags(&e, timed ? cudaEventDefault : cudaEventDisableTiming));
+        pool_ev.push_back(e);
     }
-    const std::vector<cudaEvent_t>& ev = c->events;
+    const std::vector<cudaEvent_t>& ev = pool_ev;
     size_t evi = 0;
+    // per work item: stage k spans [span[b][2k], span[b][2k+1]] (timed calls)
+    std::vector<std::array<cudaEvent_t, 6>> span(timed ? nwork : 0);
     std::vector<cudaEvent_t> slot_free(s1, nullptr);  // decode slot j reusable after its last finish
     double h2d = 0.0;
     int launches0 = static_cast<int>(g_launches.load());
@@ -796,9 +826,33 @@ qrm_status detect_host_impl(qrm_ctx* c, const uint8_t* images, int64_t count, in
         cudaStream_t cs = c->streams[s0 + s1 + b % s2];
         const int slot = lane;
         Workspace& W = c->ws[1 + slot];
-        const uint8_t* src = dimg + first * stride;
+        const uint8_t* src = dimg ? dimg + first * stride : nullptr;
         int64_t src_stride = stride;
+        cudaEvent_t e_in = ev[evi++], e_mid = ev[evi++], e_done = ev[evi++];
+        cudaEvent_t t0s = nullptr, t1s = nullptr, t2s = nullptr;
+        if (timed) {
+            t0s = ev[evi++];
+            t1s = ev[evi++];
+            t2s = ev[evi++];
+            span[b] = {t0s, e_in, t1s, e_mid, t2s, e_done};
+        }
         if (slot_free[slot]) QRM_CUDA(cudaStreamWaitEvent(xs, slot_free[slot], 0));
+        if (t0s) QRM_CUDA(cudaEventRecord(t0s, xs));
+        const long long ld0 = load_ns[0] * cnt, ld1 = load_ns[1] * cnt, ld2 = load_ns[2] * cnt;
+        // stage 1 (decode) on ds once stage 0 is done, stage 2 (complete + return) on cs
+        auto start_decode = [&]() -> qrm_status {
+            QRM_CUDA(cudaStreamWaitEvent(ds, e_in, 0));
+            if (t1s) QRM_CUDA(cudaEventRecord(t1s, ds));
+            return QRM_OK;
+        };
+        auto finish_return = [&]() -> qrm_status {
+            QRM_CUDA(cudaMemcpyAsync(hout + first, c->d_records + first, sizeof(qrm_record) * cnt,
+                                     cudaMemcpyDeviceToHost, cs));
+            if (ld2 > 0) QRM_LAUNCH(launch_stage_load(ld2, cs));
+            QRM_CUDA(cudaEventRecord(e_done, cs));
+            slot_free[slot] = e_done;
+            return QRM_OK;
+        };
         if (mode == 2 || mode == 3) {
             // stage 0. Mode 3: the transfer kernel pulls the first `nz` windows
             // over PCIe (zero-copy) while the CPU workers copy the others into
@@ -807,7 +861,6 @@ qrm_status detect_host_impl(qrm_ctx* c, const uint8_t* images, int64_t count, in
             // 50.9 GB/s half and half). Mode 2: all windows through staging.
             const int K = c->K;
             const int64_t nz = mode == 3 ? std::min(cnt, static_cast<int64_t>(c->hybrid_fraction * cnt)) : 0;
-            if ((s = ensure(W.stage, W.stage_cap, mb * K)) != QRM_OK) return s;
             WindowSource hs{};
             hs.base = src;
             hs.image_stride = stride;
@@ -837,7 +890,7 @@ qrm_status detect_host_impl(qrm_ctx* c, const uint8_t* images, int64_t count, in
                         int tx, ty;
                         select_tile(kWorkingSize, kWorkingSize, l, cfg.tile_strategy, cfg.tile_seed,
                                     first_draw + static_cast<uint64_t>(img), tx, ty);
-                        const uint8_t* src0 = images + img * stride + static_cast<int64_t>(yo + ty) * pitch +
+                        const uint8_t* src0 = image_at(img) + static_cast<int64_t>(yo + ty) * pitch +
                                               static_cast<int64_t>(xo + tx) * 3;
                         uint8_t* dst = hst + i * K;
                         if (rowb == 192) {
@@ -859,14 +912,14 @@ qrm_status detect_host_impl(qrm_ctx* c, const uint8_t* images, int64_t count, in
                                          cps));
             }
             h2d += static_cast<double>(K) * cnt;
-            cudaEvent_t e_in = ev[evi++];
+            if (ld0 > 0) QRM_LAUNCH(launch_stage_load(ld0, xs));
             QRM_CUDA(cudaEventRecord(e_in, xs));
-            QRM_CUDA(cudaStreamWaitEvent(ds, e_in, 0));
-            if (mode == 3) {
+            if (mode == 3) {  // the staged share arrives on the copy stream
                 cudaEvent_t e_cp = ev[evi++];
                 QRM_CUDA(cudaEventRecord(e_cp, cps));
                 QRM_CUDA(cudaStreamWaitEvent(ds, e_cp, 0));
             }
+            if ((s = start_decode()) != QRM_OK) return s;
             WindowSource ws = hs;
             ws.base = W.stage;
             ws.image_stride = K;
@@ -874,14 +927,11 @@ qrm_status detect_host_impl(qrm_ctx* c, const uint8_t* images, int64_t count, in
             ws.direct = 0;
             ws.x_off = 0;
             ws.y_off = 0;
-            cudaEvent_t e_mid = ev[evi++];
-            if ((s = run_detect(c, W, ws, cnt, c->d_records + first, nullptr, nullptr, ds, e_mid, cs)) != QRM_OK)
+            // the windows are complete by event order (e_in); only a decode precedes on ds
+            if ((s = run_detect(c, W, ws, cnt, c->d_records + first, nullptr, nullptr, ds, e_mid, cs, false, ld1,
+                                t2s)) != QRM_OK)
                 return s;
-            QRM_CUDA(cudaMemcpyAsync(out + first, c->d_records + first, sizeof(qrm_record) * cnt,
-                                     cudaMemcpyDeviceToHost, cs));
-            cudaEvent_t e_done = ev[evi++];
-            QRM_CUDA(cudaEventRecord(e_done, cs));
-            slot_free[slot] = e_done;
+            if ((s = finish_return()) != QRM_OK) return s;
             continue;
         }
         if (mode == 0 && direct_ok(c, src, w, h, stride) && (3 * c->l) % 16 == 0) {
@@ -901,22 +951,19 @@ qrm_status detect_host_impl(qrm_ctx* c, const uint8_t* images, int64_t count, in
             hs.first_draw = first_draw + static_cast<uint64_t>(first);
             if ((s = fetch_stage(c, hs, w, h, cnt, W.stage, xs)) != QRM_OK) return s;
             h2d += static_cast<double>(c->K) * cnt;
-            cudaEvent_t e_in = ev[evi++];
+            if (ld0 > 0) QRM_LAUNCH(launch_stage_load(ld0, xs));
             QRM_CUDA(cudaEventRecord(e_in, xs));
-            QRM_CUDA(cudaStreamWaitEvent(ds, e_in, 0));
+            if ((s = start_decode()) != QRM_OK) return s;
             WindowSource ws = hs;
             ws.base = W.stage;
             ws.image_stride = c->K;
             ws.pitch = 3 * c->l;
             ws.direct = 0;
-            cudaEvent_t e_mid = ev[evi++];
-            if ((s = run_detect(c, W, ws, cnt, c->d_records + first, nullptr, nullptr, ds, e_mid, cs)) != QRM_OK)
+            // the windows are complete by event order (e_in); only a decode precedes on ds
+            if ((s = run_detect(c, W, ws, cnt, c->d_records + first, nullptr, nullptr, ds, e_mid, cs, false, ld1,
+                                t2s)) != QRM_OK)
                 return s;
-            QRM_CUDA(cudaMemcpyAsync(out + first, c->d_records + first, sizeof(qrm_record) * cnt,
-                                     cudaMemcpyDeviceToHost, cs));
-            cudaEvent_t e_done = ev[evi++];
-            QRM_CUDA(cudaEventRecord(e_done, cs));
-            slot_free[slot] = e_done;
+            if ((s = finish_return()) != QRM_OK) return s;
             continue;
         }
         if (mode == 1) {
@@ -929,29 +976,39 @@ qrm_status detect_host_impl(qrm_ctx* c, const uint8_t* images, int64_t count, in
         } else {
             h2d += static_cast<double>(c->K) * cnt;  // window bytes read over PCIe by the decode kernel
         }
-        cudaEvent_t e_in = ev[evi++];
+        if (ld0 > 0) QRM_LAUNCH(launch_stage_load(ld0, xs));
         QRM_CUDA(cudaEventRecord(e_in, xs));
-        QRM_CUDA(cudaStreamWaitEvent(ds, e_in, 0));
         if (slot_free[slot]) QRM_CUDA(cudaStreamWaitEvent(ds, slot_free[slot], 0));
-        cudaEvent_t e_mid = ev[evi++];
-        // stage 1 (decode) on ds, stage 2 (complete + return) on cs
+        if ((s = start_decode()) != QRM_OK) return s;
         if ((s = detect_uniform(c, W, src, cnt, w, h, src_stride, first_draw + static_cast<uint64_t>(first),
-                                c->d_records + first, nullptr, nullptr, ds, e_mid, cs)) != QRM_OK)
+                                c->d_records + first, nullptr, nullptr, ds, e_mid, cs, true, ld1, t2s)) != QRM_OK)
             return s;
-        QRM_CUDA(cudaMemcpyAsync(out + first, c->d_records + first, sizeof(qrm_record) * cnt, cudaMemcpyDeviceToHost,
-                                 cs));
-        cudaEvent_t e_done = ev[evi++];
-        QRM_CUDA(cudaEventRecord(e_done, cs));
-        slot_free[slot] = e_done;
+        if ((s = finish_return()) != QRM_OK) return s;
     }
     for (int i = 0; i < nstreams; ++i) QRM_CUDA(cudaStreamSynchronize(c->streams[i]));
     if (c->copy_stream) QRM_CUDA(cudaStreamSynchronize(c->copy_stream));
+    if (hout != out) std::memcpy(out, hout, sizeof(qrm_record) * count);
     if (stats) {
         stats->wall_ms = static_cast<double>(now_ns() - t0) / 1e6;
         stats->h2d_bytes = h2d;
         stats->d2h_bytes = static_cast<double>(sizeof(qrm_record)) * count;
         stats->minibatches = static_cast<int>(nmb);
         stats->kernel_launches = static_cast<int>(g_launches.load()) - launches0;
+    }
+    if (timed) {
+        for (int64_t b = 0; b < nwork; ++b) {
+            const int64_t first = pieces ? (*pieces)[b].first : b * mb;
+            const int64_t cnt = pieces ? (*pieces)[b].count : std::min(mb, count - first);
+            for (int k = 0; k < 3; ++k) {
+                float ms = 0.f;
+                QRM_CUDA(cudaEventElapsedTime(&ms, span[b][2 * k], span[b][2 * k + 1]));
+                const int64_t ns = static_cast<int64_t>(static_cast<double>(ms) * 1e6);
+                opt.times->busy_ns[k] += ns;
+                if (opt.times->image_ns)
+                    for (int64_t i = first; i < first + cnt; ++i) opt.times->image_ns[3 * i + k] = ns;
+            }
+        }
+        opt.times->wall_ns = now_ns() - t0;
     }
     return QRM_OK;
 }
@@ -964,6 +1021,27 @@ QRM_EXPORT qrm_status qrm_detect_host(qrm_ctx* c, const uint8_t* images, int64_t
                                       int64_t stride, uint64_t first_draw, qrm_record* out, const qrm_plan* plan,
                                       int mode, qrm_host_stats* stats) {
     return detect_host_impl(c, images, count, w, h, stride, first_draw, out, plan, mode, stats, nullptr);
+}
+
+QRM_EXPORT qrm_status qrm_detect_host_timed(qrm_ctx* c, const uint8_t* images, int64_t count, int w, int h,
+                                            int64_t stride, uint64_t first_draw, qrm_record* out, const qrm_plan* plan,
+                                            int mode, const qrm_stage_load* load, qrm_stage_times* times) {
+    HostCallOpts o;
+    o.load = load;
+    o.times = times;
+    return detect_host_impl(c, images, count, w, h, stride, first_draw, out, plan, mode, nullptr, nullptr, o);
+}
+
+QRM_EXPORT qrm_status qrm_detect_host_images(qrm_ctx* c, const uint8_t* const* images, int64_t count, int w, int h,
+                                             uint64_t first_draw, qrm_record* out, const qrm_plan* plan,
+                                             const qrm_stage_load* load, qrm_stage_times* times) {
+    if (count > 0 && !images) return fail(QRM_INVALID_INPUT, "null image pointer array");
+    HostCallOpts o;
+    o.ptrs = images;
+    o.load = load;
+    o.times = times;
+    return detect_host_impl(c, nullptr, count, w, h, static_cast<int64_t>(w) * h * 3, first_draw, out, plan, 2,
+                            nullptr, nullptr, o);
 }
 
 QRM_EXPORT qrm_status qrm_detect_host_lpt(qrm_ctx* c, const uint8_t* images, int64_t count, int w, int h,
@@ -1044,6 +1122,30 @@ QRM_EXPORT qrm_status qrm_detect_host_multi(qrm_ctx* const* ctxs, int nctx, cons
     if (s != QRM_OK) return s;
     if (count > 0 && !out) return fail(QRM_INVALID_INPUT, "null record buffer");
     const int64_t t0 = now_ns();
+    if (count == 0) return QRM_OK;
+    // Register the caller's whole input and output ranges once, before the shard
+    // threads start: per-shard registration of sub-ranges of one pageable buffer
+    // would overlap at shared boundary pages (and one shard's unregister would
+    // pull the page from under its neighbour).
+    const int64_t in_bytes = (count - 1) * stride + static_cast<int64_t>(w) * h * 3;
+    bool reg_in = false, reg_out = false;
+    auto unreg = on_exit([&] {
+        if (reg_in) cudaHostUnregister(const_cast<uint8_t*>(images));
+        if (reg_out) cudaHostUnregister(out);
+    });
+    if ((s = set_device(ctxs[0]->device)) != QRM_OK) return s;
+    cudaPointerAttributes attr{};
+    if (cudaPointerGetAttributes(&attr, images) != cudaSuccess || attr.type != cudaMemoryTypeHost) {
+        cudaGetLastError();
+        QRM_CUDA(cudaHostRegister(const_cast<uint8_t*>(images), in_bytes,
+                                  cudaHostRegisterMapped | cudaHostRegisterPortable | cudaHostRegisterReadOnly));
+        reg_in = true;
+    }
+    if (cudaPointerGetAttributes(&attr, out) != cudaSuccess || attr.type != cudaMemoryTypeHost) {
+        cudaGetLastError();
+        QRM_CUDA(cudaHostRegister(out, sizeof(qrm_record) * count, cudaHostRegisterPortable));
+        reg_out = true;
+    }
     std::vector<qrm_status> st(nctx, QRM_OK);
     std::vector<std::string> err(nctx);
     std::vector<qrm_host_stats> part(nctx);
@@ -1204,14 +1306,18 @@ namespace {
 
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda).
 qrm_status tensor_map_encoder(PFN_cuTensorMapEncodeTiled_v12000* out) {
-    static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
-    if (!encode) {
+    // resolved once per process (thread-safe static initialisation)
+    static const PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
         cudaDriverEntryPointQueryResult q;
         void* fn = nullptr;
-        QRM_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
-        if (q != cudaDriverEntryPointSuccess || !fn) return fail(QRM_CUDA_ERROR, "cuTensorMapEncodeTiled unavailable");
-        encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
-    }
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess) {
+            cudaGetLastError();
+            fn = nullptr;
+        }
+        return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    }();
+    if (!encode) return fail(QRM_CUDA_ERROR, "cuTensorMapEncodeTiled unavailable");
     *out = encode;
     return QRM_OK;
 }
@@ -1241,17 +1347,12 @@ qrm_status encode_act_tmap(CUtensorMap* map, CUtensorMap* store_map, void* base,
 }
 
 // One 64->64 conv layer: the CTA-pair kernel (cta_group::2, M = 256; 237 us per
-// 1024 tiles against 285 us for the single-CTA kernel); QRM_CONV_PAIR=0 selects
-// the single-CTA variant.
-// The CTA-pair conv layer is the default; QRM_CONV_PAIR=0 selects the single-CTA one.
-bool conv_pair_enabled() {
-    const char* e = getenv("QRM_CONV_PAIR");
-    return !(e && e[0] == '0');
-}
-
-cudaError_t conv64_layer(const CUtensorMap& tmap, const CUtensorMap& tmap_out, const HiddenLayerParams& p, int sms,
-                         cudaStream_t st) {
-    return conv_pair_enabled() ? launch_conv64_pair(tmap, tmap_out, p, sms, st) : launch_conv64(tmap, tmap_out, p, sms, st);
+// 1024 tiles against 285 us for the single-CTA kernel) unless the context was
+// created with QRM_CONV_PAIR=0.
+cudaError_t conv64_layer(const qrm_ctx* c, const CUtensorMap& tmap, const CUtensorMap& tmap_out,
+                         const HiddenLayerParams& p, cudaStream_t st) {
+    return c->conv_pair ? launch_conv64_pair(tmap, tmap_out, p, c->sms, st)
+                        : launch_conv64(tmap, tmap_out, p, c->sms, st);
 }
 
 qrm_status hidden_prepare(qrm_ctx* c, uint64_t seed, int64_t tiles, cudaStream_t st) {
@@ -1308,11 +1409,10 @@ qrm_status hidden_run(qrm_ctx* c, Workspace& W, const WindowSource& src, int64_t
     for (int64_t off = 0; off < count; off += kConvChunk) {
         const int64_t n = std::min(kConvChunk, count - off);
         const WindowSource cs = slice_source(src, off, c->K);
-        const bool pair = conv_pair_enabled();
+        const bool pair = c->conv_pair;
         // the pair kernel's last layer folds the linear layer into its epilogue
         // (QRM_CONV_FUSE_LINEAR=0: channel partials + hidden_head_kernel instead)
-        const char* fl = getenv("QRM_CONV_FUSE_LINEAR");
-        const bool fuse_linear = pair && !(fl && fl[0] == '0');
+        const bool fuse_linear = pair && c->conv_fuse_linear;
         Conv0Params p0{cs, n, c->K, H.w0, H.bias, H.act[0]};
         QRM_LAUNCH(launch_conv0(p0, H.tmap_st[0], c->sms, st));
         for (int j = 1; j < kHiddenLayers; ++j) {
@@ -1328,7 +1428,7 @@ qrm_status hidden_run(qrm_ctx* c, Workspace& W, const WindowSource& src, int64_t
                 lp.wl = H.wl;
                 lp.nbits = c->nbits;
             }
-            QRM_LAUNCH(conv64_layer(H.tmap[(j - 1) & 1], H.tmap_st[j & 1], lp, c->sms, st));
+            QRM_LAUNCH(conv64_layer(c, H.tmap[(j - 1) & 1], H.tmap_st[j & 1], lp, st));
         }
         HeadParams hp{};
         hp.pool = H.pool;
@@ -1461,7 +1561,7 @@ QRM_EXPORT qrm_status qrm_hidden_debug_activation(qrm_ctx* c, const uint8_t* ima
         lp.act_out = lp.last ? nullptr : H.act[j & 1];
         lp.pool_out = lp.last ? H.pool : nullptr;
         lp.tiles = count;
-        QRM_LAUNCH(conv64_layer(H.tmap[(j - 1) & 1], H.tmap_st[j & 1], lp, c->sms, st));
+        QRM_LAUNCH(conv64_layer(c, H.tmap[(j - 1) & 1], H.tmap_st[j & 1], lp, st));
     }
     if (stop_after == kHiddenLayers - 1)
         QRM_CUDA(cudaMemcpyAsync(out, H.pool, sizeof(float) * kHiddenBlocksPerTile * 64 * count,

@@ -26,9 +26,11 @@
 // decoder and verify in registers, so one launch produces final records.
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdlib>
 
 #include "qrm_device.cuh"
+#include "qrm_launch.h"
 #include "qrm_rs.cuh"
 #include "qrm_types.h"
 #include "qrm_window.cuh"
@@ -203,7 +205,6 @@ __global__ void __launch_bounds__(kCorrThreads, 1) corr_detect_kernel(const __gr
     const int tid = threadIdx.x;
     const int warp = tid >> 5;
     const int lane = tid & 31;
-    dbg_mark(p, 0, tid);
     const uint32_t S = cluster_nctarank();  // 1 without a cluster launch
     const uint32_t rank = cluster_ctarank();
     const int tile_m = p.tile_m;  // images in this tile (<= 128): tiles are balanced over the SMs
@@ -230,7 +231,6 @@ __global__ void __launch_bounds__(kCorrThreads, 1) corr_detect_kernel(const __gr
     tc_fence_after();
     const uint32_t tmem = sm.tmem_base;
     const int rows_per = kCorrM / static_cast<int>(S);
-    dbg_mark(p, 1, tid);
 
     if (warp < 4) {
         // ------------------------------------------------------ producer --
@@ -247,6 +247,7 @@ __global__ void __launch_bounds__(kCorrThreads, 1) corr_detect_kernel(const __gr
         const int row_bytes = 3 * p.src.l;
         const int pitch = p.src.direct ? p.src.pitch : row_bytes;
         const uint32_t ring_u32 = smem_u32(ring);
+        if (p.wait_inputs) griddep_wait();  // the preceding kernel may have written the windows
         // K offset of this thread's 16 B, as (tile row, column) — stepped, no division per stage.
         int kbyte = kc_begin * kCorrKC + c * 16;
         int trow = kbyte / row_bytes;
@@ -256,7 +257,6 @@ __global__ void __launch_bounds__(kCorrThreads, 1) corr_detect_kernel(const __gr
         for (int it = 0; it < kchunks; ++it) {
             const int s = it % kCorrStages;
             mbar_wait(&sm.empty[s], ((it / kCorrStages) & 1) ^ 1);
-            if (p.dbg_stages && tid == 0 && blockIdx.x < 8 && it < 128) p.dbg_stages[blockIdx.x * 256 + it] = clock64();
             const uint32_t a_s = ring_u32 + s * kCorrStageBytes;
             const uint32_t b_s = a_s + kCorrABytes;
             if (kbyte < p.K) {
@@ -285,9 +285,7 @@ __global__ void __launch_bounds__(kCorrThreads, 1) corr_detect_kernel(const __gr
         cp_async_wait<0>();
 
         // ------------------------------------------------------ epilogue --
-        dbg_mark(p, 2, tid);
         mbar_wait(&sm.accum_full, 0);
-        dbg_mark(p, 3, tid);
         tc_fence_after();
         uint32_t acc[kCorrN];
 #pragma unroll
@@ -299,14 +297,12 @@ __global__ void __launch_bounds__(kCorrThreads, 1) corr_detect_kernel(const __gr
         }
         tmem_ld_wait();
         tc_fence_before();
-        dbg_mark(p, 4, tid);
 
         const int row = warp * 32 + lane;
         if (S == 1) {
             griddep_wait();  // the previous completion kernel is done with records / the pending list
             const int64_t img = m0 + row;
             if (row < tile_m && img < p.count) finish_image(p, sm, tl, img, acc);
-            dbg_mark(p, 5, tid);
         } else {
             // push this partial row to its owner CTA: slot `rank`, local row
             const uint32_t owner = static_cast<uint32_t>(row / rows_per);
@@ -319,7 +315,6 @@ __global__ void __launch_bounds__(kCorrThreads, 1) corr_detect_kernel(const __gr
 #pragma unroll
             for (int q = 0; q < kCorrN / 4; ++q)
                 st_cluster_v4(dst + 16 * q, acc[4 * q], acc[4 * q + 1], acc[4 * q + 2], acc[4 * q + 3]);
-            dbg_mark(p, 5, tid);
         }
     } else if (warp == 4) {
         // ------------------------------------------------------ MMA issuer --
@@ -329,7 +324,6 @@ __global__ void __launch_bounds__(kCorrThreads, 1) corr_detect_kernel(const __gr
             for (int it = 0; it < kchunks; ++it) {
                 const int s = it % kCorrStages;
                 mbar_wait(&sm.full[s], (it / kCorrStages) & 1);
-                if (p.dbg_stages && blockIdx.x < 8 && it < 128) p.dbg_stages[blockIdx.x * 256 + 128 + it] = clock64();
                 // The stage's bytes are in smem (written through the generic
                 // proxy by cp.async); order them before the async-proxy MMA reads.
                 fence_proxy_async_smem();
@@ -352,7 +346,6 @@ __global__ void __launch_bounds__(kCorrThreads, 1) corr_detect_kernel(const __gr
     }
     if (S > 1) {
         cluster_sync_all();  // every partial row has landed in its owner's smem
-        dbg_mark(p, 6, tid);
         if (tid < rows_per) {
             griddep_wait();  // the previous completion kernel is done with records / the pending list
             uint32_t acc[kCorrN];
@@ -374,7 +367,6 @@ __global__ void __launch_bounds__(kCorrThreads, 1) corr_detect_kernel(const __gr
             if (row < tile_m && img < p.count) finish_image(p, sm, tl, img, acc);
         }
     }
-    dbg_mark(p, 7, tid);
     __syncthreads();
     if (sm.nties > 0) finish_ties(p, sm, tl, warp, lane);  // rare: exact zero correlations
     if (warp == 4) {
@@ -402,10 +394,14 @@ static cudaLaunchConfig_t corr_config(unsigned grid, unsigned S, cudaStream_t st
     return cfg;
 }
 
-// Co-resident clusters of size S (one CTA per SM; clusters must fit a GPC).
+// Co-resident clusters of size S (one CTA per SM; clusters must fit a GPC),
+// cached per device.
 static int max_active_clusters(unsigned S, int sms) {
-    static int cache[9] = {0};
-    if (cache[S] == 0) {
+    static std::atomic<int> table[kMaxDevices][9];
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::atomic<int>* cache = table[dev < kMaxDevices ? dev : 0];
+    if (cache[S].load() == 0) {
         cudaLaunchAttribute attr[2];
         cudaLaunchConfig_t cfg = corr_config(S * 64, S, nullptr, attr);
         int n = 0;
@@ -413,21 +409,23 @@ static int max_active_clusters(unsigned S, int sms) {
             cudaGetLastError();
             n = sms / static_cast<int>(S);
         }
-        cache[S] = n;
+        cache[S].store(n);
     }
-    return cache[S];
+    return cache[S].load();
 }
 
 cudaError_t launch_corr_detect(const DetectParams& p_in, int sm_count, cudaStream_t st) {
-    static bool configured = false;
-    if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(corr_detect_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    // function attributes belong to each device's context: set once per device
+    static PerDeviceOnce once;
+    cudaError_t e = once.run([] {
+        cudaError_t r = cudaFuncSetAttribute(corr_detect_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              static_cast<int>(kCorrSmemBytes));
-        if (e != cudaSuccess) return e;
-        e = cudaFuncSetAttribute(corr_detect_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        if (r != cudaSuccess) return r;
+        cudaFuncSetAttribute(corr_detect_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
         cudaGetLastError();
-        configured = true;
-    }
+        return cudaSuccess;
+    });
+    if (e != cudaSuccess) return e;
     const int64_t tiles128 = (p_in.count + kCorrM - 1) / kCorrM;
     if (tiles128 == 0) return cudaSuccess;
     // Split K over a cluster when there are too few 128-image tiles to give
@@ -435,10 +433,8 @@ cudaError_t launch_corr_detect(const DetectParams& p_in, int sm_count, cudaStrea
     const int sms = sm_count > 0 ? sm_count : 148;
     unsigned S = 1;
     while (S < 4 && tiles128 * S * 2 <= sms && (p_in.K_pad / kCorrKC) >= static_cast<int>(8 * S * 2)) S *= 2;
-    if (const char* env = getenv("QRM_CORR_KSPLIT")) {  // experiment hook
-        const int v = atoi(env);
-        if (v == 1 || v == 2 || v == 4 || v == 8) S = static_cast<unsigned>(v);
-    }
+    if (p_in.ksplit == 1 || p_in.ksplit == 2 || p_in.ksplit == 4 || p_in.ksplit == 8)
+        S = static_cast<unsigned>(p_in.ksplit);  // forced (context's QRM_CORR_KSPLIT)
     // Balance: whole waves of co-resident clusters, each tile <= 128 images.
     const int64_t per_wave = max_active_clusters(S, sms);
     const int64_t waves = (tiles128 + per_wave - 1) / per_wave;

@@ -12,9 +12,12 @@
 #include <chrono>
 #include <cmath>
 #include <cstring>
+#include <memory>
 #include <numeric>
+#include <thread>
 
 #include "host_code.hpp"
+#include "host_pool.hpp"
 #include "qrmark/api.hpp"
 #include "qrmark_gpu.h"
 #include "sched_host.hpp"
@@ -478,17 +481,26 @@ SpreadSpectrumCodec::SpreadSpectrumCodec(const WatermarkKey& key, int tile_size)
     if (key.n_bits <= 0) throw InvalidInput("payload width must be positive");
     if (key.alpha < 0.0) throw InvalidInput("alpha must be nonnegative");
     if (tile_size <= 0) throw InvalidInput("tile size must be positive");
-    patterns_.resize(static_cast<size_t>(key.n_bits) * samples());
-    for (int i = 0; i < key.n_bits; ++i)
-        for (size_t px = 0; px < samples(); ++px)
-            patterns_[i * samples() + px] = (rng_word(key.seed, static_cast<uint64_t>(i), px) & 1) ? 1 : -1;
+}
+// The host copy of the +-1 planes (stego.cpp:22-26) is built on first use:
+// extraction runs on the device planes, and only residual / embed /
+// pattern_correlation read these (detect_batch's per-call context never does).
+const int8_t* SpreadSpectrumCodec::planes() const {
+    std::call_once(host_planes_->once, [&] {
+        auto& v = host_planes_->v;
+        v.resize(static_cast<size_t>(key_.n_bits) * samples());
+        for (int i = 0; i < key_.n_bits; ++i)
+            for (size_t px = 0; px < samples(); ++px)
+                v[i * samples() + px] = (rng_word(key_.seed, static_cast<uint64_t>(i), px) & 1) ? 1 : -1;
+    });
+    return host_planes_->v.data();
 }
 std::vector<float> SpreadSpectrumCodec::residual(const BitVec& bits) const {
     if (static_cast<int>(bits.size()) != key_.n_bits) throw InvalidInput("payload bit-length mismatch");
     std::vector<float> d(samples(), 0.0f);
     for (int i = 0; i < key_.n_bits; ++i) {
         const float s = bits[i] ? 1.0f : -1.0f;
-        const int8_t* p = patterns_.data() + i * samples();
+        const int8_t* p = planes() + i * samples();
         for (size_t px = 0; px < d.size(); ++px) d[px] += s * p[px];
     }
     return d;
@@ -511,8 +523,8 @@ SoftBits SpreadSpectrumCodec::extract(const ImageBuffer& tile) const {
     return s;
 }
 double SpreadSpectrumCodec::pattern_correlation(int i, int j) const {
-    const int8_t* a = patterns_.data() + i * samples();
-    const int8_t* b = patterns_.data() + j * samples();
+    const int8_t* a = planes() + i * samples();
+    const int8_t* b = planes() + j * samples();
     double acc = 0.0;
     for (size_t px = 0; px < samples(); ++px) acc += static_cast<double>(a[px]) * b[px];
     return acc / static_cast<double>(samples());
@@ -654,9 +666,29 @@ static std::string cache_key(const BitVec& raw) {
         if (raw[i]) key[i / 8] |= static_cast<char>(1 << (i % 8));
     return key;
 }
+// The codebook keeps its keys in least-recently-used order (lru_), so eviction
+// pops from the front instead of scanning the map twice per call as the
+// reference does (detect.cpp:115-128). The evicted set is the same: entries
+// past stale_after are exactly a prefix of that order (the oldest), and the
+// capacity rule then removes the oldest one at a time.
 bool CorrectionCache::record(const BitVec& raw, const std::optional<DecodeResult>& decoded) {
+    return record(raw, [&] { return decoded; });
+}
+bool CorrectionCache::record(const BitVec& raw, const std::function<std::optional<DecodeResult>()>& decoded_on_miss) {
+    return record_key(cache_key(raw), decoded_on_miss);
+}
+bool CorrectionCache::record_packed(uint64_t raw_word, int n_bits,
+                                    const std::function<std::optional<DecodeResult>()>& decoded_on_miss) {
+    // the same key as cache_key(unpack(raw_word)): bit i of the BitVec is word
+    // bit n-1-i, packed LSB-first into bytes
+    uint64_t lsb_first = 0;
+    for (int i = 0; i < n_bits; ++i) lsb_first |= ((raw_word >> (n_bits - 1 - i)) & 1ull) << i;
+    std::string key(static_cast<size_t>((n_bits + 7) / 8), '\0');
+    for (size_t b = 0; b < key.size(); ++b) key[b] = static_cast<char>((lsb_first >> (8 * b)) & 0xff);
+    return record_key(std::move(key), decoded_on_miss);
+}
+bool CorrectionCache::record_key(std::string key, const std::function<std::optional<DecodeResult>()>& decoded_on_miss) {
     // correct()'s bookkeeping with the decode already done on the GPU
-    std::string key = cache_key(raw);
     std::lock_guard<std::mutex> lk(mu_);
     ++tick_;
     ++lookups_;
@@ -664,12 +696,10 @@ bool CorrectionCache::record(const BitVec& raw, const std::optional<DecodeResult
     auto it = map_.find(key);
     if (it != map_.end()) {
         ++hits_;
-        it->second.last_access = tick_;
+        touch_locked(it->second);
         return true;
     }
-    auto [jt, ins] = map_.try_emplace(std::move(key));
-    jt->second.result = decoded;
-    jt->second.last_access = tick_;
+    insert_locked(std::move(key), decoded_on_miss());
     evict_locked();
     return false;
 }
@@ -683,28 +713,32 @@ std::pair<std::optional<DecodeResult>, bool> CorrectionCache::correct(const BitV
         auto it = map_.find(key);
         if (it != map_.end()) {
             ++hits_;
-            it->second.last_access = tick_;
+            touch_locked(it->second);
             return {it->second.result, true};
         }
     }
     auto res = bw_decode(raw, params);
     std::lock_guard<std::mutex> lk(mu_);
-    auto [it, ins] = map_.try_emplace(std::move(key));
-    it->second.result = res;
-    it->second.last_access = tick_;
+    insert_locked(std::move(key), res);
     evict_locked();
     return {std::move(res), false};
 }
+void CorrectionCache::touch_locked(Entry& e) {
+    lru_.splice(lru_.end(), lru_, e.pos);
+    e.last_access = tick_;
+}
+void CorrectionCache::insert_locked(std::string key, std::optional<DecodeResult> result) {
+    auto [it, ins] = map_.try_emplace(std::move(key));
+    if (ins) it->second.pos = lru_.insert(lru_.end(), it->first);
+    it->second.result = std::move(result);
+    touch_locked(it->second);
+}
 void CorrectionCache::evict_locked() {
-    for (auto it = map_.begin(); it != map_.end();) {
-        if (tick_ - it->second.last_access > cfg_.stale_after) it = map_.erase(it);
-        else ++it;
-    }
-    while (map_.size() > cfg_.capacity) {
-        auto old = map_.begin();
-        for (auto it = map_.begin(); it != map_.end(); ++it)
-            if (it->second.last_access < old->second.last_access) old = it;
-        map_.erase(old);
+    while (!lru_.empty()) {
+        auto it = map_.find(lru_.front());
+        if (tick_ - it->second.last_access <= cfg_.stale_after && map_.size() <= cfg_.capacity) break;
+        map_.erase(it);
+        lru_.pop_front();
     }
 }
 size_t CorrectionCache::size() const {
@@ -725,11 +759,6 @@ void write_ppm(const ImageBuffer& img, const std::filesystem::path& path) {
     check(qrm_ppm_write(path.string().c_str(), img.bytes.data(), img.width, img.height));
 }
 
-struct GpuContext {
-    qrm_ctx* h = nullptr;
-    std::vector<qrm_ctx*> shards;  // one per DetectionConfig::devices entry (multi-device batches)
-};
-
 static qrm_config gpu_config(const DetectionConfig& cfg) {
     qrm_config c{};
     c.symbol_bits = cfg.code.field->bits();
@@ -745,6 +774,89 @@ static qrm_config gpu_config(const DetectionConfig& cfg) {
     return c;
 }
 
+namespace {
+
+// Process-wide pool of C-ABI contexts keyed by (device, configuration). The
+// reference builds a fresh DetectionContext for every detect_batch call
+// (detect.cpp:254). Its device counterpart -- pattern planes, RS tables, the
+// streams, the pinned window-staging ring (~50 MB per decode slot) -- depends
+// only on the configuration, so a context returned by one call is handed to
+// the next call with the same key instead of being rebuilt. A context is used
+// by one DetectionContext at a time. Idle contexts are bounded; the pool is
+// never destroyed (tearing down CUDA state during static destruction is unsafe).
+class CtxPool {
+public:
+    static CtxPool& get() {
+        static CtxPool* p = new CtxPool;
+        return *p;
+    }
+    static std::string key_of(const DetectionConfig& cfg, int device) {
+        std::string k = std::to_string(device) + "/" + std::to_string(cfg.code.field->bits()) + "/" +
+                        std::to_string(cfg.code.n) + "/" + std::to_string(cfg.code.k) + "/" +
+                        std::to_string(cfg.tile.size) + "/" + std::to_string(static_cast<int>(cfg.tile.strategy)) +
+                        "/" + std::to_string(cfg.tile.seed) + "/" + std::to_string(cfg.key.seed) + "/" +
+                        std::to_string(cfg.key.alpha) + "/" + std::to_string(cfg.fpr_target) + "/" +
+                        std::to_string(static_cast<int>(cfg.extractor)) + "/" + std::to_string(cfg.conv_weight_seed) +
+                        "/";
+        for (uint8_t b : cfg.key_message) k.push_back(static_cast<char>('0' + (b & 1)));
+        return k;
+    }
+    qrm_ctx* acquire(const DetectionConfig& cfg, int device, const std::string& key) {
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            for (auto it = idle_.begin(); it != idle_.end(); ++it)
+                if (it->first == key) {
+                    qrm_ctx* c = it->second;
+                    idle_.erase(it);
+                    return c;
+                }
+        }
+        qrm_config c = gpu_config(cfg);
+        qrm_ctx* h = nullptr;
+        check(qrm_ctx_create(device, &c, &h));
+        if (cfg.extractor == ExtractorKind::conv) {
+            const qrm_status s = qrm_ctx_set_extractor(h, QRM_EXTRACTOR_CONV, cfg.conv_weight_seed);
+            if (s != QRM_OK) {
+                qrm_ctx_destroy(h);
+                raise(s);
+            }
+        }
+        return h;
+    }
+    void release(const std::string& key, qrm_ctx* c) {
+        if (!c) return;
+        qrm_ctx* evict = nullptr;
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            idle_.emplace_back(key, c);
+            if (idle_.size() > kMaxIdle) {
+                evict = idle_.front().second;
+                idle_.erase(idle_.begin());
+            }
+        }
+        if (evict) qrm_ctx_destroy(evict);
+    }
+
+private:
+    static constexpr size_t kMaxIdle = 8;
+    std::mutex mu_;
+    std::vector<std::pair<std::string, qrm_ctx*>> idle_;  // oldest first
+};
+
+}  // namespace
+
+struct GpuContext {
+    std::string key;
+    qrm_ctx* h = nullptr;
+    // one per DetectionConfig::devices entry (multi-device batches), created on first use
+    std::vector<std::string> shard_keys;
+    std::vector<qrm_ctx*> shards;
+    ~GpuContext() {
+        for (size_t i = 0; i < shards.size(); ++i) CtxPool::get().release(shard_keys[i], shards[i]);
+        CtxPool::get().release(key, h);
+    }
+};
+
 DetectionContext::DetectionContext(const DetectionConfig& cfg, int device)
     : cfg_(cfg),
       codec_(cfg.key, cfg.tile.size),
@@ -752,28 +864,26 @@ DetectionContext::DetectionContext(const DetectionConfig& cfg, int device)
       tau_message_(verify_threshold(cfg.code.message_bits(), cfg.fpr_target)),
       tau_raw_(verify_threshold(cfg.code.codeword_bits(), cfg.fpr_target)),
       cache_(cfg.cache),
-      gpu_(new GpuContext) {
+      gpu_(nullptr) {
+    // validate before any device state is taken (a throw here leaks nothing)
     if (cfg.key.n_bits != cfg.code.codeword_bits())
         throw InvalidInput("key payload width must equal the codeword width");
     if (cfg.rs_workers < 1) throw InvalidInput("rs_workers must be >= 1");
     if (cfg.fpr_target <= 0.0 || cfg.fpr_target >= 1.0) throw InvalidInput("fpr target must be in (0, 1)");
-    qrm_config c = gpu_config(cfg_);
-    qrm_status s = qrm_ctx_create(device, &c, &gpu_->h);
-    if (s == QRM_OK && cfg.extractor == ExtractorKind::conv) {
-        s = qrm_ctx_set_extractor(gpu_->h, QRM_EXTRACTOR_CONV, cfg.conv_weight_seed);
-        if (s != QRM_OK) qrm_ctx_destroy(gpu_->h);
-    }
-    if (s != QRM_OK) {
-        delete gpu_;
-        raise(s);
-    }
+    auto g = std::make_unique<GpuContext>();
+    g->key = CtxPool::key_of(cfg_, device);
+    g->h = CtxPool::get().acquire(cfg_, device, g->key);
+    gpu_ = g.release();
 }
-DetectionContext::~DetectionContext() {
-    if (gpu_) {
-        for (qrm_ctx* s : gpu_->shards) qrm_ctx_destroy(s);
-        qrm_ctx_destroy(gpu_->h);
-    }
-    delete gpu_;
+DetectionContext::~DetectionContext() { delete gpu_; }
+
+// Host threads that turn device records into DetectionRecords (large batches).
+static qrm::HostPool& conversion_pool() {
+    static qrm::HostPool* pool = [] {
+        const unsigned hc = std::thread::hardware_concurrency();
+        return new qrm::HostPool(static_cast<int>(std::max(1u, std::min(hc ? hc - 2 : 1u, 15u))));
+    }();
+    return *pool;
 }
 
 static DetectionRecord to_record(const qrm_record& r, size_t index, const DetectionConfig& cfg) {
@@ -790,53 +900,89 @@ static DetectionRecord to_record(const qrm_record& r, size_t index, const Detect
     return d;
 }
 
+// The reference's StreamPlan (sched.hpp:26-34) as the executor's plan: streams
+// per stage, and the mini-batch = the largest stage mini-batch (detect_batch
+// sizes its queues by the largest entry, detect.cpp:266).
+static qrm_plan to_gpu_plan(const StreamPlan* plan) {
+    qrm_plan pl{{1, 2, 1}, {4096, 4096, 4096}};
+    if (!plan) return pl;
+    if (plan->streams.size() != 3) throw InvalidInput("detect pipeline expects a 3-stage plan");
+    for (int k = 0; k < 3; ++k) pl.streams[k] = std::max(1, plan->streams[k]);
+    if (!plan->minibatch.empty()) {
+        const int mb = std::max(1, *std::max_element(plan->minibatch.begin(), plan->minibatch.end()));
+        for (int k = 0; k < 3; ++k) pl.minibatch[k] = mb;
+    }
+    return pl;
+}
+
 std::vector<DetectionRecord> DetectionContext::detect_many(std::span<const ImageBuffer> images, uint64_t first_draw,
-                                                           const StreamPlan* plan) {
+                                                           const StreamPlan* plan, const SyntheticStageLoad* load,
+                                                           DeskReport* report) {
+    const auto wall0 = std::chrono::steady_clock::now();
     const int64_t n = static_cast<int64_t>(images.size());
+    const qrm_plan pl = to_gpu_plan(plan);
     std::vector<DetectionRecord> out(n);
+    if (report) {
+        *report = DeskReport{};
+        for (int k = 0; k < 3; ++k) report->stage_workers[k] = pl.streams[k];
+    }
     if (n == 0) return out;
     bool uniform = true;
     for (const ImageBuffer& im : images) {
         if (im.form != PixelForm::byte) throw InvalidInput("preprocess expects byte form");
         uniform = uniform && im.width == images[0].width && im.height == images[0].height;
     }
+    const int w = images[0].width, h = images[0].height;
+    const bool direct = uniform && std::min(w, h) >= kWorkingSize;  // no bilinear upscale
+    qrm_stage_load ld{{0, 0, 0}};
+    if (load) {
+        ld.ns[0] = load->preprocess_ns;
+        ld.ns[1] = load->extract_ns;
+        ld.ns[2] = load->correct_ns;
+        if (!direct && (ld.ns[0] || ld.ns[1] || ld.ns[2]))
+            throw InvalidInput("a synthetic stage load needs same-size images of at least 256 px (the stage pipeline)");
+    }
     std::vector<qrm_record> rec(n);
-    if (uniform) {
-        const int w = images[0].width, h = images[0].height;
-        const size_t bytes = static_cast<size_t>(w) * h * 3;
-        uint8_t* pinned = nullptr;
-        cuda_check(cudaHostAlloc(&pinned, bytes * n, cudaHostAllocMapped), "cudaHostAlloc");
-        for (int64_t i = 0; i < n; ++i) std::memcpy(pinned + i * bytes, images[i].bytes.data(), bytes);
-        qrm_plan pl{{1, 2, 1}, {4096, 4096, 4096}};
-        if (plan) {
-            if (plan->streams.size() != 3 || plan->minibatch.size() != 3)
-                throw InvalidInput("detect pipeline expects a 3-stage plan");
-            for (int k = 0; k < 3; ++k) {
-                pl.streams[k] = std::max(1, plan->streams[k]);
-                pl.minibatch[k] = std::max(1, plan->minibatch[k]);
-            }
-        }
-        qrm_status s = QRM_OK;
-        if (cfg_.devices.size() > 1 && gpu_->shards.empty()) {
-            // one context per listed device, created on first use
-            qrm_config c = gpu_config(cfg_);
+    std::vector<int64_t> image_ns(direct ? 3 * n : 0, 0);
+    int64_t busy[3] = {0, 0, 0};
+    if (direct) {
+        // Only each image's l x l window leaves its ImageBuffer: the context's host
+        // workers gather the windows into its pinned staging ring (no whole-image
+        // copy, no per-call pinned allocation), the copy engine moves them.
+        std::vector<const uint8_t*> ptrs(n);
+        for (int64_t i = 0; i < n; ++i) ptrs[i] = images[i].bytes.data();
+        if (cfg_.devices.size() > 1 && gpu_->shards.empty())
             for (int dev : cfg_.devices) {
-                qrm_ctx* x = nullptr;
-                if ((s = qrm_ctx_create(dev, &c, &x)) != QRM_OK) break;
-                gpu_->shards.push_back(x);
-                if (cfg_.extractor == ExtractorKind::conv &&
-                    (s = qrm_ctx_set_extractor(x, QRM_EXTRACTOR_CONV, cfg_.conv_weight_seed)) != QRM_OK)
-                    break;
+                gpu_->shard_keys.push_back(CtxPool::key_of(cfg_, dev));
+                gpu_->shards.push_back(nullptr);
+                gpu_->shards.back() = CtxPool::get().acquire(cfg_, dev, gpu_->shard_keys.back());
             }
+        const int nctx = gpu_->shards.size() > 1 ? static_cast<int>(gpu_->shards.size()) : 1;
+        // contiguous shards with global draw indices, one host thread per device
+        std::vector<qrm_status> st(nctx, QRM_OK);
+        std::vector<std::string> err(nctx);
+        std::vector<qrm_stage_times> tm(nctx);
+        auto run = [&](int i) {
+            const int64_t b = n * i / nctx, e = n * (i + 1) / nctx;
+            tm[i] = qrm_stage_times{0, {0, 0, 0}, image_ns.data() + 3 * b};
+            qrm_ctx* c = nctx > 1 ? gpu_->shards[i] : gpu_->h;
+            st[i] = qrm_detect_host_images(c, ptrs.data() + b, e - b, w, h, first_draw + static_cast<uint64_t>(b),
+                                           rec.data() + b, &pl, &ld, &tm[i]);
+            if (st[i] != QRM_OK) err[i] = qrm_last_error();
+        };
+        std::vector<std::thread> th;
+        for (int i = 1; i < nctx; ++i) th.emplace_back(run, i);
+        run(0);
+        for (auto& t : th) t.join();
+        for (int i = 0; i < nctx; ++i) {
+            if (st[i] != QRM_OK) {
+                const std::string msg = (nctx > 1 ? "shard " + std::to_string(i) + ": " : std::string()) + err[i];
+                if (st[i] == QRM_INVALID_INPUT) throw InvalidInput(msg);
+                if (st[i] == QRM_INFEASIBLE) throw InfeasibleConfig(msg);
+                throw CudaUnavailable(msg);
+            }
+            for (int k = 0; k < 3; ++k) busy[k] += tm[i].busy_ns[k];
         }
-        if (s == QRM_OK && gpu_->shards.size() > 1)
-            s = qrm_detect_host_multi(gpu_->shards.data(), static_cast<int>(gpu_->shards.size()), pinned, n, w, h,
-                                      static_cast<int64_t>(bytes), first_draw, rec.data(), &pl, 0, nullptr);
-        else if (s == QRM_OK)
-            s = qrm_detect_host(gpu_->h, pinned, n, w, h, static_cast<int64_t>(bytes), first_draw, rec.data(), &pl, 0,
-                                nullptr);  // mapped-window transfer
-        cudaFreeHost(pinned);
-        check(s);
     } else {
         std::vector<const uint8_t*> ptrs(n);
         std::vector<int> ws(n), hs(n);
@@ -845,18 +991,47 @@ std::vector<DetectionRecord> DetectionContext::detect_many(std::span<const Image
             ws[i] = images[i].width;
             hs[i] = images[i].height;
         }
+        const auto r0 = std::chrono::steady_clock::now();
         check(qrm_detect_ragged(gpu_->h, ptrs.data(), ws.data(), hs.data(), n, first_draw, rec.data()));
+        // one fused gather + decode + correct call: the whole span is the decode stage's
+        busy[1] = std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now() - r0).count();
     }
-    for (int64_t i = 0; i < n; ++i) out[i] = to_record(rec[i], first_draw + i, cfg_);
-    if (cfg_.cache.enabled) {
-        // DetectionRecord::cache_hit as the reference reports it (detect.cpp:326-333):
-        // the context's codebook sees the words in index order
-        for (int64_t i = 0; i < n; ++i) {
-            std::optional<DecodeResult> d;
-            if (out[i].corrected) d = DecodeResult{*out[i].corrected, rs_encode(*out[i].corrected, cfg_.code),
-                                                   out[i].errors_corrected};
-            out[i].cache_hit = cache_.record(out[i].raw_bits, d);
+    // Records -> DetectionRecords on the conversion pool while this thread
+    // replays the codebook (index order, as the reference's cache sees the words
+    // with one correct worker; it reads only the packed words).
+    auto convert = [&](int64_t b, int64_t e) {
+        for (int64_t i = b; i < e; ++i) {
+            out[i] = to_record(rec[i], first_draw + i, cfg_);
+            if (direct) out[i].stage_ns = StageLatencies{image_ns[3 * i], image_ns[3 * i + 1], image_ns[3 * i + 2]};
         }
+    };
+    std::vector<uint8_t> hit(cfg_.cache.enabled ? n : 0, 0);
+    auto replay = [&] {
+        const int nb = cfg_.code.codeword_bits(), kb = cfg_.code.message_bits();
+        for (int64_t i = 0; i < n; ++i)
+            hit[i] = cache_.record_packed(rec[i].raw, nb, [&]() -> std::optional<DecodeResult> {
+                if (rec[i].status != QRM_REC_DECODED) return std::nullopt;  // stored only on a miss
+                BitVec m = unpack(rec[i].msg, kb);
+                BitVec cw = rs_encode(m, cfg_.code);
+                return DecodeResult{std::move(m), std::move(cw), rec[i].errors};
+            });
+    };
+    if (n >= 1024) {
+        std::thread rt;
+        if (cfg_.cache.enabled) rt = std::thread(replay);
+        conversion_pool().parallel_for(n, 256, convert);
+        if (rt.joinable()) rt.join();
+    } else {
+        convert(0, n);
+        if (cfg_.cache.enabled) replay();
+    }
+    if (cfg_.cache.enabled)
+        for (int64_t i = 0; i < n; ++i) out[i].cache_hit = hit[i] != 0;
+    if (report) {
+        report->wall_ns =
+            std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now() - wall0).count();
+        for (int k = 0; k < 3; ++k) report->stage_busy_ns[k] = busy[k];
+        report->items = static_cast<size_t>(n);
     }
     return out;
 }
@@ -870,19 +1045,13 @@ DetectionRecord detect_one(const ImageBuffer& img, const DetectionConfig& cfg) {
 }
 
 std::vector<DetectionRecord> detect_batch(std::span<const ImageBuffer> images, const DetectionConfig& cfg,
-                                          const StreamPlan* plan, const SyntheticStageLoad*, DeskReport* report) {
+                                          const StreamPlan* plan, const SyntheticStageLoad* load, DeskReport* report) {
     DetectionContext ctx(cfg);
-    if (plan && plan->streams.size() != 3) throw InvalidInput("detect pipeline expects a 3-stage plan");
-    const auto t0 = std::chrono::steady_clock::now();
-    auto recs = ctx.detect_many(images, 0, plan);
-    if (report) {
-        *report = DeskReport{};
-        report->wall_ns = std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now() - t0).count();
-        if (plan)
-            for (int k = 0; k < 3; ++k) report->stage_workers[k] = plan->streams[k];
-        report->items = images.size();
+    if (images.empty()) {  // as the reference: no plan check for an empty batch (detect.cpp:256-260)
+        if (report) *report = DeskReport{};
+        return {};
     }
-    return recs;
+    return ctx.detect_many(images, 0, plan, load, report);
 }
 
 // --------------------------------------------------------------------- sim

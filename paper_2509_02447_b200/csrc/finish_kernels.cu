@@ -234,6 +234,25 @@ cudaError_t launch_gather_windows(const GatherDesc* descs, int64_t count, int l,
     return cudaGetLastError();
 }
 
+// SyntheticStageLoad on the device: holds the stream for `ns` nanoseconds (one
+// warp, global timer), the stage-stream analogue of the reference's
+// synthetic_wait sleep (detect.cpp:243-245).
+__global__ void stage_load_kernel(long long ns) {
+    if (threadIdx.x != 0) return;
+    unsigned long long t0, t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    do {
+        __nanosleep(2000);
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    } while (static_cast<long long>(t - t0) < ns);
+}
+
+cudaError_t launch_stage_load(long long ns, cudaStream_t st) {
+    if (ns <= 0) return cudaSuccess;
+    stage_load_kernel<<<1, 32, 0, st>>>(ns);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_resample(const GatherDesc& d, int out_w, int out_h, int normalize, void* out, cudaStream_t st) {
     const int64_t n = static_cast<int64_t>(out_w) * out_h * 3;
     int64_t blocks = (n + 255) / 256;

@@ -28,6 +28,7 @@
 
 #include "qrm_device.cuh"
 #include "qrm_hidden.h"
+#include "qrm_launch.h"
 #include "qrm_rs.cuh"
 #include "qrm_types.h"
 #include "qrm_window.cuh"
@@ -768,13 +769,12 @@ cudaError_t launch_conv0(const Conv0Params& p, const CUtensorMap& tmap_out, int 
 
 cudaError_t launch_conv64(const CUtensorMap& tmap, const CUtensorMap& tmap_out, const HiddenLayerParams& p,
                           int sm_count, cudaStream_t st) {
-    static bool configured = false;
-    if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(conv64_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             static_cast<int>(kHSmemBytes));
-        if (e != cudaSuccess) return e;
-        configured = true;
-    }
+    static PerDeviceOnce once;  // function attributes are per device context
+    const cudaError_t e = once.run([] {
+        return cudaFuncSetAttribute(conv64_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(kHSmemBytes));
+    });
+    if (e != cudaSuccess) return e;
     const int64_t nblocks = p.tiles * kHBlocks;
     int64_t grid = sm_count > 0 ? sm_count : 148;
     if (grid > nblocks) grid = nblocks;
@@ -785,13 +785,12 @@ cudaError_t launch_conv64(const CUtensorMap& tmap, const CUtensorMap& tmap_out, 
 
 cudaError_t launch_conv64_pair(const CUtensorMap& tmap, const CUtensorMap& tmap_out, const HiddenLayerParams& p,
                                int sm_count, cudaStream_t st) {
-    static bool configured = false;
-    if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(conv64_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             static_cast<int>(kPSmemBytes));
-        if (e != cudaSuccess) return e;
-        configured = true;
-    }
+    static PerDeviceOnce once;  // function attributes are per device context
+    const cudaError_t e = once.run([] {
+        return cudaFuncSetAttribute(conv64_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(kPSmemBytes));
+    });
+    if (e != cudaSuccess) return e;
     const int64_t npb = p.tiles * kPairBlocks;
     int64_t pairs = (sm_count > 0 ? sm_count : 148) / 2;
     if (pairs > npb) pairs = npb;

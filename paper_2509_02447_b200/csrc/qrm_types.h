@@ -66,8 +66,9 @@ struct DetectParams {
     int32_t tau_msg, tau_raw;
     int32_t fuse_t1;    // epilogue may run the t=1 RS decoder itself
     int32_t tile_m;     // images per decode tile (<= 128 TMEM lanes); set by the launcher
-    unsigned long long* dbg_times;  // nullable: per-CTA phase timestamps (globaltimer ns), 8 per CTA
-    long long* dbg_stages;          // nullable: CTAs 0-7, [cta][2][128] clock64 at producer issue / MMA full
+    int32_t wait_inputs;  // 1: the windows may be written by the preceding kernel on the stream, so the
+                          // producers griddep_wait() before their first load (no overlap with that kernel)
+    int32_t ksplit;       // launcher: forced split-K cluster size (0: automatic)
     uint64_t key_cw, key_msg;
     const int8_t* patterns;   // [64][K_pad] s8, rows >= nbits zero
     const int32_t* colsum;    // [64] sum_px P_i[px]

@@ -19,13 +19,4 @@ __device__ __forceinline__ const uint8_t* window_base(const WindowSource& s, int
            static_cast<int64_t>(s.x_off + tx) * 3;
 }
 
-// Diagnostics: per-CTA phase timestamps (thread 0), only when requested.
-__device__ __forceinline__ void dbg_mark(const DetectParams& p, int phase, int tid) {
-    if (p.dbg_times && tid == 0) {
-        unsigned long long t;
-        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-        p.dbg_times[static_cast<int64_t>(blockIdx.x) * 8 + phase] = t;
-    }
-}
-
 }  // namespace qrm

@@ -21,6 +21,7 @@
 #include "qrmark/stego.hpp"
 #include "qrmark/tiling.hpp"
 #include "qrmark/transforms.hpp"
+#include "qrmark_gpu.h"
 
 using namespace qrmark;
 
@@ -199,6 +200,37 @@ static void host_tiling_sched() {
 }
 
 // ------------------------------------------------------------------- gpu
+// CorrectionCache's LRU eviction (detect.cpp:86-128) against the C-ABI's
+// replay (qrm_cache_hits, pinned to the reference's own JSON output in
+// tests/test_formats.py), with eviction by capacity and by staleness.
+static void host_cache() {
+    CounterRng rng(31, 0);
+    for (auto [cap, stale] : {std::pair<size_t, uint64_t>{4, 1u << 20}, {16, 7}, {3, 2}, {4096, 1u << 20}}) {
+        CorrectionCache cache(CacheConfig{true, cap, stale}), packed(CacheConfig{true, cap, stale});
+        std::vector<qrm_record> recs(3000);
+        std::vector<uint8_t> want(recs.size());
+        for (size_t i = 0; i < recs.size(); ++i) {
+            // a skewed stream: a few hot words and a long tail
+            const uint64_t r = rng.next();
+            const uint64_t word = (r & 3) ? (r >> 8) % 9 : (r >> 8) % 400;
+            recs[i] = qrm_record{};
+            recs[i].raw = word;
+        }
+        CHECK(qrm_cache_hits(recs.data(), static_cast<int64_t>(recs.size()), static_cast<int64_t>(cap), stale,
+                             want.data()) == QRM_OK);
+        size_t hits = 0;
+        for (size_t i = 0; i < recs.size(); ++i) {
+            BitVec raw(60);
+            for (int b = 0; b < 60; ++b) raw[b] = (recs[i].raw >> (59 - b)) & 1;
+            const bool h = cache.record(raw, std::optional<DecodeResult>{});
+            CHECK(h == (want[i] != 0));
+            CHECK(packed.record_packed(recs[i].raw, 60, [] { return std::optional<DecodeResult>{}; }) == h);
+            hits += h;
+        }
+        CHECK(cache.hits() == hits && cache.size() <= cap);
+    }
+}
+
 static void gpu_rs() {
     CounterRng rng(22, 0);
     for (const char* name : {"gf16-15-12", "gf256-dynamic"}) {
@@ -368,6 +400,31 @@ static void gpu_stego_detect() {
         CHECK(semantic_equal(rp[i], rq[i]));
         CHECK(semantic_equal(rp[i], ctx.detect_one(pos[i], i)));
     }
+    // DeskReport and StageLatencies are filled from the stage streams' events
+    CHECK(rep.wall_ns > 0 && rep.stage_busy_ns[0] > 0 && rep.stage_busy_ns[1] > 0 && rep.stage_busy_ns[2] > 0);
+    for (const auto& r : rq) CHECK(r.stage_ns.preprocess_ns > 0 && r.stage_ns.extract_ns > 0 && r.stage_ns.correct_ns > 0);
+    // SyntheticStageLoad holds each stage's stream load_ns per image (detect.cpp:304, 318, 336)
+    {
+        SyntheticStageLoad load{0, 200000, 50000};  // 0.2 ms per image on decode, 0.05 ms on correct
+        StreamPlan one{{1, 1, 1}, {8}, 0.0};         // minibatch of any length: its largest entry (detect.cpp:266)
+        DeskReport lr;
+        auto rl = detect_batch(pos, cfg, &one, &load, &lr);
+        CHECK(lr.stage_busy_ns[1] >= static_cast<int64_t>(pos.size()) * 200000);
+        CHECK(lr.stage_busy_ns[2] >= static_cast<int64_t>(pos.size()) * 50000);
+        CHECK(lr.wall_ns >= static_cast<int64_t>(pos.size()) * 200000);
+        for (size_t i = 0; i < rl.size(); ++i) {
+            CHECK(semantic_equal(rl[i], rp[i]));
+            CHECK(rl[i].stage_ns.extract_ns >= 8 * 200000);  // its mini-batch of 8 held the decode stream
+        }
+        CHECK_THROWS_AS(detect_batch(std::vector<ImageBuffer>{pos[0], noise_image(4, 300, 200)}, cfg, nullptr, &load),
+                        InvalidInput);
+    }
+    {
+        StreamPlan bad{{1, 1}, {4, 4}, 0.0};
+        CHECK_THROWS_AS(detect_batch(pos, cfg, &bad), InvalidInput);
+        DeskReport er;
+        CHECK(detect_batch(std::vector<ImageBuffer>{}, cfg, &bad, nullptr, &er).empty() && er.items == 0);
+    }
     // ragged inputs through the same entry
     std::vector<ImageBuffer> mixed = {pos[0], noise_image(4, 300, 200), noise_image(5, 100, 90)};
     auto rm = detect_batch(mixed, cfg);
@@ -432,7 +489,7 @@ int main(int argc, char** argv) {
         bool gpu;
         void (*fn)();
     } cases[] = {{"gf", false, host_gf},          {"rs_encode", false, host_rs_encode},
-                 {"tiling_sched", false, host_tiling_sched}, {"ppm", false, host_ppm}, {"rs_gpu", true, gpu_rs},
+                 {"tiling_sched", false, host_tiling_sched}, {"ppm", false, host_ppm}, {"cache", false, host_cache}, {"rs_gpu", true, gpu_rs},
                  {"image_gpu", true, gpu_image},  {"stego_detect_gpu", true, gpu_stego_detect},
                  {"conv_detect_gpu", true, gpu_conv_detect}};
     for (auto& c : cases) {
