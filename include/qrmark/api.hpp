@@ -385,15 +385,22 @@ public:
     // The same for a packed raw word (n_bits <= 64, bit 0 of the BitVec in the word's top used bit).
     bool record_packed(uint64_t raw_word, int n_bits,
                        const std::function<std::optional<DecodeResult>()>& decoded_on_miss);
+    // A batch of packed words in index order under one lock (hit[i] = 0 / 1);
+    // word i at raw_words[i * word_stride].
+    void record_packed_batch(const uint64_t* raw_words, size_t count, size_t word_stride, int n_bits,
+                             const std::function<std::optional<DecodeResult>(size_t)>& decoded_on_miss, uint8_t* hit);
     size_t size() const;
     uint64_t hits() const { return hits_; }
     uint64_t lookups() const { return lookups_; }
 
 private:
+    struct LruNode {
+        std::string key;
+        uint64_t last_access = 0;
+    };
     struct Entry {
         std::optional<DecodeResult> result;
-        uint64_t last_access = 0;
-        std::list<std::string>::iterator pos;  // place in lru_
+        std::list<LruNode>::iterator pos;  // place (and last access tick) in lru_
     };
     bool record_key(std::string key, const std::function<std::optional<DecodeResult>()>& decoded_on_miss);
     void touch_locked(Entry& e);
@@ -402,7 +409,7 @@ private:
     CacheConfig cfg_;
     mutable std::mutex mu_;
     std::unordered_map<std::string, Entry> map_;
-    std::list<std::string> lru_;  // keys, least recently used first
+    std::list<LruNode> lru_;  // least recently used first
     uint64_t tick_ = 0, hits_ = 0, lookups_ = 0;
 };
 

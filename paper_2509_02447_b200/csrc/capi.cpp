@@ -197,6 +197,7 @@ struct qrm_ctx {
     std::vector<cudaEvent_t> timing_events;  // the same with timing, for calls that report stage spans
     double hybrid_fraction = 0.5;        // mode 3: share of each mini-batch fetched zero-copy
     int64_t stage_piece = 512;           // modes 2/3: windows gathered per H2D
+    int64_t stage_grain = 32;            // modes 2/3: windows per host-worker task
     double decode_ms_per_image = 0.0;  // from the last warm-up profile (Algorithm 2 latencies)
     int extractor = QRM_EXTRACTOR_SPREAD_SPECTRUM;  // qrm_ctx_set_extractor
     bool input_overlap = false;  // qrm_ctx_set_input_overlap
@@ -469,6 +470,7 @@ QRM_EXPORT qrm_status qrm_ctx_create(int device, const qrm_config* cfg, qrm_ctx*
     if (const char* e = getenv("QRM_CONV_PAIR")) c->conv_pair = e[0] != '0';
     if (const char* e = getenv("QRM_CONV_FUSE_LINEAR")) c->conv_fuse_linear = e[0] != '0';
     if (const char* e = getenv("QRM_STAGE_PIECE")) c->stage_piece = std::max<int64_t>(16, atoll(e));
+    if (const char* e = getenv("QRM_STAGE_GRAIN")) c->stage_grain = std::max<int64_t>(1, atoll(e));
     for (int i = 0; i < kbits; ++i) c->key_msg = (c->key_msg << 1) | (c->key_message[i] & 1);
     c->key_cw = encode_packed(c->m, c->n, c->k, c->key_msg);
     c->tau_msg = verify_threshold(kbits, cfg->fpr_target);
@@ -884,7 +886,7 @@ qrm_status detect_host_impl(qrm_ctx* c, const uint8_t* images, int64_t count, in
             const int64_t piece = c->stage_piece;
             for (int64_t p0 = 0; p0 < cnt - nz; p0 += piece) {
                 const int64_t p1 = std::min(cnt - nz, p0 + piece);
-                c->pool->parallel_for(p1 - p0, 32, [&](int64_t j0, int64_t j1) {
+                c->pool->parallel_for(p1 - p0, c->stage_grain, [&](int64_t j0, int64_t j1) {
                     for (int64_t i = p0 + j0; i < p0 + j1; ++i) {
                         const int64_t img = first + nz + i;
                         int tx, ty;

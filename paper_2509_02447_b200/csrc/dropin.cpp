@@ -677,15 +677,43 @@ bool CorrectionCache::record(const BitVec& raw, const std::optional<DecodeResult
 bool CorrectionCache::record(const BitVec& raw, const std::function<std::optional<DecodeResult>()>& decoded_on_miss) {
     return record_key(cache_key(raw), decoded_on_miss);
 }
-bool CorrectionCache::record_packed(uint64_t raw_word, int n_bits,
-                                    const std::function<std::optional<DecodeResult>()>& decoded_on_miss) {
+static std::string packed_key(uint64_t raw_word, int n_bits) {
     // the same key as cache_key(unpack(raw_word)): bit i of the BitVec is word
     // bit n-1-i, packed LSB-first into bytes
     uint64_t lsb_first = 0;
     for (int i = 0; i < n_bits; ++i) lsb_first |= ((raw_word >> (n_bits - 1 - i)) & 1ull) << i;
     std::string key(static_cast<size_t>((n_bits + 7) / 8), '\0');
     for (size_t b = 0; b < key.size(); ++b) key[b] = static_cast<char>((lsb_first >> (8 * b)) & 0xff);
-    return record_key(std::move(key), decoded_on_miss);
+    return key;
+}
+bool CorrectionCache::record_packed(uint64_t raw_word, int n_bits,
+                                    const std::function<std::optional<DecodeResult>()>& decoded_on_miss) {
+    return record_key(packed_key(raw_word, n_bits), decoded_on_miss);
+}
+void CorrectionCache::record_packed_batch(const uint64_t* raw_words, size_t count, size_t word_stride, int n_bits,
+                                          const std::function<std::optional<DecodeResult>(size_t)>& decoded_on_miss,
+                                          uint8_t* hit) {
+    std::lock_guard<std::mutex> lk(mu_);  // one lock for the whole batch
+    uint64_t prev = 0;
+    std::string key;
+    for (size_t i = 0; i < count; ++i) {
+        const uint64_t w = raw_words[i * word_stride];
+        if (i == 0 || w != prev) key = packed_key(w, n_bits);
+        prev = w;
+        ++tick_;
+        ++lookups_;
+        evict_locked();
+        auto it = map_.find(key);
+        if (it != map_.end()) {
+            ++hits_;
+            touch_locked(it->second);
+            hit[i] = 1;
+            continue;
+        }
+        insert_locked(key, decoded_on_miss(i));
+        evict_locked();
+        hit[i] = 0;
+    }
 }
 bool CorrectionCache::record_key(std::string key, const std::function<std::optional<DecodeResult>()>& decoded_on_miss) {
     // correct()'s bookkeeping with the decode already done on the GPU
@@ -725,19 +753,20 @@ std::pair<std::optional<DecodeResult>, bool> CorrectionCache::correct(const BitV
 }
 void CorrectionCache::touch_locked(Entry& e) {
     lru_.splice(lru_.end(), lru_, e.pos);
-    e.last_access = tick_;
+    e.pos->last_access = tick_;
 }
 void CorrectionCache::insert_locked(std::string key, std::optional<DecodeResult> result) {
     auto [it, ins] = map_.try_emplace(std::move(key));
-    if (ins) it->second.pos = lru_.insert(lru_.end(), it->first);
+    if (ins) it->second.pos = lru_.insert(lru_.end(), LruNode{it->first, tick_});
     it->second.result = std::move(result);
     touch_locked(it->second);
 }
 void CorrectionCache::evict_locked() {
+    // the oldest entry is at the front; no map lookup unless it goes
     while (!lru_.empty()) {
-        auto it = map_.find(lru_.front());
-        if (tick_ - it->second.last_access <= cfg_.stale_after && map_.size() <= cfg_.capacity) break;
-        map_.erase(it);
+        const LruNode& old = lru_.front();
+        if (tick_ - old.last_access <= cfg_.stale_after && map_.size() <= cfg_.capacity) break;
+        map_.erase(old.key);
         lru_.pop_front();
     }
 }
@@ -1007,14 +1036,16 @@ std::vector<DetectionRecord> DetectionContext::detect_many(std::span<const Image
     };
     std::vector<uint8_t> hit(cfg_.cache.enabled ? n : 0, 0);
     auto replay = [&] {
-        const int nb = cfg_.code.codeword_bits(), kb = cfg_.code.message_bits();
-        for (int64_t i = 0; i < n; ++i)
-            hit[i] = cache_.record_packed(rec[i].raw, nb, [&]() -> std::optional<DecodeResult> {
+        const int kb = cfg_.code.message_bits();
+        cache_.record_packed_batch(
+            &rec[0].raw, static_cast<size_t>(n), sizeof(qrm_record) / sizeof(uint64_t), cfg_.code.codeword_bits(),
+            [&](size_t i) -> std::optional<DecodeResult> {
                 if (rec[i].status != QRM_REC_DECODED) return std::nullopt;  // stored only on a miss
                 BitVec m = unpack(rec[i].msg, kb);
                 BitVec cw = rs_encode(m, cfg_.code);
                 return DecodeResult{std::move(m), std::move(cw), rec[i].errors};
-            });
+            },
+            hit.data());
     };
     if (n >= 1024) {
         std::thread rt;

@@ -228,6 +228,11 @@ static void host_cache() {
             hits += h;
         }
         CHECK(cache.hits() == hits && cache.size() <= cap);
+        CorrectionCache batch(CacheConfig{true, cap, stale});
+        std::vector<uint8_t> bh(recs.size(), 2);
+        batch.record_packed_batch(&recs[0].raw, recs.size(), sizeof(qrm_record) / sizeof(uint64_t), 60,
+                                  [](size_t) { return std::optional<DecodeResult>{}; }, bh.data());
+        CHECK(bh == want && batch.hits() == hits);
     }
 }
 
