@@ -230,7 +230,7 @@ def hidden_submetric(ctx, pool, world, max_over_ranks, stream, batch=BATCH, reps
         recs_pin = torch.empty((batch, q.RECORD_DTYPE.itemsize), dtype=torch.uint8, pin_memory=True)
         recs = recs_pin.numpy().view(q.RECORD_DTYPE).reshape(-1)
         # one mini-batch: the conv layers' fixed costs amortise better than the
-        # fetch/decode overlap smaller mini-batches buy (scripts/e2e_conv.py)
+        # fetch/decode overlap smaller mini-batches buy (round-1 probe)
         plan = ([1, 1, 1], [batch] * 3)
         H, W = host_pool.shape[1], host_pool.shape[2]
         with q.DetectionContext(cfg, device=ctx.device) as cctx:
@@ -426,7 +426,7 @@ def main():
         return st
 
     e2e = {}
-    ctx.set_transfer_split(0.7)  # mode 3: 70 % zero-copy, 30 % host-staged (scripts/host_modes_native.cpp sweep)
+    ctx.set_transfer_split(0.7)  # mode 3: 70 % zero-copy, 30 % host-staged (round-1 sweep)
     for mode in (2, 3, 0, 1):
         for i in range(args.warmup):
             e2e_step(i, mode)

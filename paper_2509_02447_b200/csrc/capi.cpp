@@ -859,7 +859,7 @@ qrm_status detect_host_impl(qrm_ctx* c, const uint8_t* images, int64_t count, in
             // stage 0. Mode 3: the transfer kernel pulls the first `nz` windows
             // over PCIe (zero-copy) while the CPU workers copy the others into
             // pinned staging for one copy-engine H2D on the copy stream; the two
-            // share the link (scripts/pcie_probe.cu: 47.8 GB/s zero-copy alone,
+            // share the link (round-1 PCIe probe: 47.8 GB/s zero-copy alone,
             // 50.9 GB/s half and half). Mode 2: all windows through staging.
             const int K = c->K;
             const int64_t nz = mode == 3 ? std::min(cnt, static_cast<int64_t>(c->hybrid_fraction * cnt)) : 0;

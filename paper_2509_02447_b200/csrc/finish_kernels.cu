@@ -148,7 +148,7 @@ __global__ void gather_windows_kernel(const GatherDesc* __restrict__ descs, int6
 // mapped (zero-copy) pinned host memory into contiguous device windows. Only
 // the window crosses PCIe (3 l^2 of the 3 w h bytes). Plain 16-B loads, NB per
 // thread in flight before any store, keep enough reads outstanding to fill the
-// link (measured ~48 GB/s of the ~55 GB/s copy-engine rate, scripts/pcie_probe.cu).
+// link (measured ~48 GB/s of the ~55 GB/s copy-engine rate, round-1 PCIe probe in profiles/r1_pcie_probe.log).
 template <int NB>
 __global__ void __launch_bounds__(256) fetch_windows_kernel(const WindowSource src, int64_t count, int K,
                                                             uint8_t* __restrict__ out) {
