@@ -139,6 +139,11 @@ def bench_config(world: int) -> dict:
                   "4 x 50 MB of tile windows per rotation > 126 MB L2)"}
 
 
+def oracle_reference():
+    import oracle
+    return oracle.Reference()
+
+
 def cpu_rs_baseline(words_np, threads):
     import oracle
     ref = oracle.Reference()
@@ -498,6 +503,52 @@ def main():
     assert bool((ne[small] == ne_true[small]).all())
     cpu_words = words[:1_000_000].cpu().numpy().view(np.uint64)  # CPU-reference RS sample
     del words, cw, ne, msg
+    # GF(2^8) codes (north-star item 3): gf256-dynamic(48) = (8,6) packed, (12,8)
+    # t=2 and (255,223) t=16 as symbol rows, device stress words (e <= t for
+    # 90%, t+1..t+2 for 10%), the segmented warp decoder.
+    rs_gf256 = {}
+    cpu_sym_samples = {}
+    gf_cases = (("gf256-dynamic-48 (8,6) t=1, packed", q.resolve_profile("gf256-dynamic", 48), None, 10_000_000),
+                ("(12,8) t=2, symbols", q.CodeParams.make(8, 12, 8), "sym", 4_000_000),
+                ("(255,223) t=16, symbols", q.CodeParams.make(8, 255, 223), "sym", 400_000))
+    for name, gcode, kind, nw in gf_cases:
+        nw = min(nw, args.rs_words)
+        if kind is None:
+            _, gw, gne_true = q.rs_stress_words(gcode, 3030 + rank, nw)
+            gcw, gne = torch.empty_like(gw), torch.empty(nw, dtype=torch.int8, device=dev)
+            run = lambda: q.bw_decode_packed(gcode, gw, gcw, gne, algo=2)
+            in_b, out_b = 8, 9
+        else:
+            gtrue, gw, gne_true = q.rs_stress_symbols(gcode, 3030 + rank, nw)
+            gcw, gne = torch.empty_like(gw), torch.empty(nw, dtype=torch.int8, device=dev)
+            run = lambda: q.bw_decode_symbols_into(gcode, gw, gcw, gne)
+            in_b, out_b = gcode.n, gcode.n + 1
+        for _ in range(3):
+            run()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        reps = 10
+        a.record(stream)
+        for _ in range(reps):
+            run()
+        b.record(stream)
+        torch.cuda.synchronize()
+        gms = max_over_ranks(a.elapsed_time(b) / reps)
+        small = gne_true <= gcode.t
+        assert bool((gne[small] == gne_true[small]).all())
+        if kind is not None:
+            assert bool((gcw[small] == gtrue[small]).all())
+            cpu_sym_samples[name] = (gcode, gw[: (2000 if gcode.n > 100 else 200_000)].cpu().numpy())
+            del gtrue
+        else:
+            cpu_sym_samples[name] = (gcode, gw[:1_000_000].cpu().numpy().view(np.uint64))
+        rs_gf256[name] = {"words": nw, "codewords_per_s": world * nw / (gms / 1e3), "ms": gms,
+                          "bytes_per_codeword": in_b + out_b,
+                          "achieved_gbs": (in_b + out_b) * nw / (gms / 1e3) / 1e9,
+                          "decoder": "rs_seg_packed_kernel" if kind is None else "rs_seg_symbols_kernel"}
+        del gw, gcw, gne, gne_true
+    rs["gf256"] = rs_gf256
+
 
     # Learned extractor (SURVEY 8(d) "learned path"): 9 x conv3x3 64ch on
     # tcgen05 kind::f16 + pool + head + RS, same 4096-image batches.
@@ -569,6 +620,14 @@ def main():
             nthreads = os.cpu_count() or 1
             rs["cpu_reference_codewords_per_s"] = cpu_rs_baseline(cpu_words, nthreads)
             rs["cpu_reference_sample"] = f"1,000,000 stress words, bw_decode on {nthreads} threads"
+            ref_o = oracle_reference()
+            for name, (gcode, sample) in cpu_sym_samples.items():
+                if sample.dtype == np.uint64:
+                    _, _, wall = ref_o.bw_decode_packed(gcode.m, gcode.n, gcode.k, sample, threads=nthreads)
+                else:
+                    _, _, wall = ref_o.bw_decode_symbols_mt(gcode.m, gcode.n, gcode.k, sample, threads=nthreads)
+                rs["gf256"][name]["cpu_reference_codewords_per_s"] = sample.shape[0] / (wall / 1e9)
+                rs["gf256"][name]["cpu_reference_sample"] = f"{sample.shape[0]:,} stress words, bw_decode on {nthreads} threads"
         except Exception as exc:  # the reference library may be absent
             cpu = {"value": None, "unit": "images/s", "cores": os.cpu_count(), "kind": "reference",
                    "sample": f"unavailable: {exc}"}

@@ -350,6 +350,12 @@ QRM_EXPORT qrm_status qrm_rs_decode_symbols_device(int m, int n, int k, const ui
  * its codeword with e injected symbol errors (e <= t for 90%, t+1..3 for 10%). */
 QRM_EXPORT qrm_status qrm_rs_stress_device(int m, int n, int k, uint64_t seed, int64_t count, uint64_t* msg,
                                            uint64_t* words, int8_t* nerr_true, void* stream);
+/* RS stress words for symbol codes (any n <= 255, m <= 8, k*(n-k) <= 96 KiB):
+ * per word the codeword of a random message (true_cw, [count][n] symbols),
+ * the received word with e injected symbol errors (recv) and e (nerr_true);
+ * e <= t for 90% of words, t+1..t+2 for 10%. */
+QRM_EXPORT qrm_status qrm_rs_stress_symbols_device(int m, int n, int k, uint64_t seed, int64_t count,
+                                                   uint8_t* true_cw, uint8_t* recv, int8_t* nerr_true, void* stream);
 /* rs_encode (rs.cpp:78-91) on the host, packed (n*m <= 64). */
 QRM_EXPORT qrm_status qrm_rs_encode_packed(int m, int n, int k, uint64_t message, uint64_t* codeword);
 /* verify_threshold (detect.cpp:31-66). */

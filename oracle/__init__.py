@@ -385,6 +385,9 @@ class Reference(_Common):
                                            C.POINTER(C.c_uint64), C.POINTER(C.c_int8)]
         L.ref_bw_decode_symbols.argtypes = [C.c_int, C.c_int, C.c_int, C.POINTER(C.c_uint8), C.c_int64,
                                             C.POINTER(C.c_uint8), C.POINTER(C.c_int8)]
+        L.ref_bw_decode_symbols_mt.restype = C.c_int64
+        L.ref_bw_decode_symbols_mt.argtypes = [C.c_int, C.c_int, C.c_int, C.POINTER(C.c_uint8), C.c_int64, C.c_int,
+                                               C.POINTER(C.c_uint8), C.POINTER(C.c_int8)]
         L.ref_verify_threshold.argtypes = [C.c_int, C.c_double, C.POINTER(C.c_int)]
         L.ref_synthetic_image.argtypes = [C.c_uint64, C.c_int, C.c_int, C.POINTER(C.c_uint8)]
         L.ref_make_corpus.argtypes = [C.c_uint64, C.c_int64, C.c_int, C.c_int, C.c_uint64, C.c_double, C.c_int,
@@ -459,6 +462,16 @@ class Reference(_Common):
         ne = np.zeros(w.shape, np.int8)
         wall = self.lib.ref_bw_decode_packed(m, n, k, _p(w, C.c_uint64), w.size, threads, _p(cw, C.c_uint64),
                                              _p(ne, C.c_int8))
+        if wall < 0:
+            raise ValueError(self.last_error())
+        return cw, ne, wall
+
+    def bw_decode_symbols_mt(self, m, n, k, recv, threads=1):
+        """bw_decode over symbol rows on `threads` host threads -> (cw, nerr, wall_ns)."""
+        r = np.ascontiguousarray(recv, np.uint8).reshape(-1, n)
+        cw = np.zeros_like(r)
+        ne = np.zeros(r.shape[0], np.int8)
+        wall = self.lib.ref_bw_decode_symbols_mt(m, n, k, _u8p(r), r.shape[0], threads, _u8p(cw), _p(ne, C.c_int8))
         if wall < 0:
             raise ValueError(self.last_error())
         return cw, ne, wall

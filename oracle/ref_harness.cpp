@@ -284,6 +284,46 @@ REF_API int ref_bw_decode_symbols(int m, int n, int k, const uint8_t* recv, int6
     });
 }
 
+// The same over `threads` host threads, returning the wall time in ns (the RS
+// CPU baseline for symbol codes, e.g. GF(2^8) (12,8) and (255,223)).
+REF_API int64_t ref_bw_decode_symbols_mt(int m, int n, int k, const uint8_t* recv, int64_t count, int threads,
+                                         uint8_t* cw_out, int8_t* nerr_out) {
+    int64_t wall = -1;
+    guarded([&] {
+        CodeParams p = code_of(m, n, k);
+        threads = std::max(1, threads);
+        std::atomic<int64_t> next{0};
+        const int64_t chunk = 1024;
+        auto worker = [&] {
+            std::vector<uint16_t> sym(n);
+            while (true) {
+                int64_t b = next.fetch_add(chunk);
+                if (b >= count) break;
+                int64_t e = std::min(count, b + chunk);
+                for (int64_t i = b; i < e; ++i) {
+                    for (int j = 0; j < n; ++j) sym[j] = recv[i * n + j];
+                    auto res = bw_decode(symbols_to_bits(sym, m), p);
+                    if (res) {
+                        auto cs = bits_to_symbols(res->codeword, m);
+                        for (int j = 0; j < n; ++j) cw_out[i * n + j] = static_cast<uint8_t>(cs[j]);
+                        nerr_out[i] = static_cast<int8_t>(res->errors_corrected);
+                    } else {
+                        std::memset(cw_out + i * n, 0, n);
+                        nerr_out[i] = -1;
+                    }
+                }
+            }
+        };
+        int64_t t0 = now_ns();
+        std::vector<std::thread> pool;
+        for (int t = 1; t < threads; ++t) pool.emplace_back(worker);
+        worker();
+        for (auto& th : pool) th.join();
+        wall = now_ns() - t0;
+    });
+    return wall;
+}
+
 REF_API int ref_verify_threshold(int n_bits, double fpr, int* tau) {
     return guarded([&] { *tau = verify_threshold(n_bits, fpr); });
 }

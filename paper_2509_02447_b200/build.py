@@ -52,7 +52,7 @@ def _run(cmd, verbose):
 def build(verbose: bool = False, ptxas_verbose: bool = False) -> str:
     os.makedirs(OBJ, exist_ok=True)
     hdrs = _headers()
-    objs = []
+    objs, jobs = [], []
     cxx = os.environ.get("CXX", shutil.which("g++") or "g++")
     for src in sorted(glob.glob(os.path.join(CSRC, "*.cu"))):
         obj = os.path.join(OBJ, os.path.basename(src) + ".o")
@@ -62,13 +62,18 @@ def build(verbose: bool = False, ptxas_verbose: bool = False) -> str:
                    "--expt-relaxed-constexpr", "-I", CSRC, "-I", INCLUDE, "-c", src, "-o", obj]
             if ptxas_verbose:
                 cmd.insert(1, "-Xptxas=-v")
-            _run(cmd, verbose or ptxas_verbose)
+            jobs.append(cmd)
     for src in sorted(glob.glob(os.path.join(CSRC, "*.cpp"))):
         obj = os.path.join(OBJ, os.path.basename(src) + ".o")
         objs.append(obj)
         if _stale(obj, [src] + hdrs):
-            _run([cxx, "-O2", "-std=c++20", "-fPIC", "-fvisibility=hidden", "-Wall", "-Wextra",
-                  "-I", CSRC, "-I", INCLUDE, "-I", os.path.join(CUDA_HOME, "include"), "-c", src, "-o", obj], verbose)
+            jobs.append([cxx, "-O2", "-std=c++20", "-fPIC", "-fvisibility=hidden", "-Wall", "-Wextra",
+                         "-I", CSRC, "-I", INCLUDE, "-I", os.path.join(CUDA_HOME, "include"), "-c", src, "-o", obj])
+    # translation units compile independently: run them concurrently
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(max(1, min(len(jobs), os.cpu_count() or 1))) as ex:
+        for f in [ex.submit(_run, cmd, verbose or ptxas_verbose) for cmd in jobs]:
+            f.result()
     if _stale(LIB, objs):
         _run([NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-Xcompiler", "-fPIC", "-lpthread"], verbose)
     return LIB

@@ -48,10 +48,13 @@ cudaError_t launch_attack_pixels(const AttackParams& p, cudaStream_t st);
 cudaError_t launch_tile_bf16(const CUtensorMap& tmap, const TileBf16Params& p, int sm_count, cudaStream_t st);
 cudaError_t launch_attack_jpeg(const AttackParams& p, cudaStream_t st);
 cudaError_t launch_attack_resample(const AttackParams& p, cudaStream_t st);
-cudaError_t launch_rs_packed(const RsTables* tab, int m, int r, int t, int algo, const uint64_t* words,
+cudaError_t launch_rs_packed(const RsTables* tab, int m, int n, int r, int t, int algo, const uint64_t* words,
                              int64_t count, uint64_t* cw, int8_t* nerr, int sm_count, cudaStream_t st);
 cudaError_t launch_rs_symbols(const RsTables* tab, int n, int t, const uint8_t* recv, int64_t count, uint8_t* cw,
                               int8_t* nerr, int sm_count, cudaStream_t st);
+cudaError_t launch_rs_stress_symbols(const RsTables* tab, const uint8_t* gpar, int k, int r, uint64_t seed,
+                                     int64_t count, uint8_t* true_cw, uint8_t* recv, int8_t* nerr_true,
+                                     cudaStream_t st);
 cudaError_t launch_rs_stress(const RsTables* tab, const uint64_t* enc_mask, uint64_t seed, int64_t count,
                              uint64_t* msg, uint64_t* words, int8_t* nerr_true, cudaStream_t st);
 cudaError_t launch_build_patterns(uint64_t seed, int nbits, int K, int K_pad, int8_t* pat, int32_t* colsum,
@@ -1219,7 +1222,7 @@ QRM_EXPORT qrm_status qrm_rs_decode_packed_device(int m, int n, int k, const uin
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    QRM_LAUNCH(launch_rs_packed(tab, m, n - k, t, algo, words, count, cw_out, nerr_out, sms, as_stream(stream)));
+    QRM_LAUNCH(launch_rs_packed(tab, m, n, n - k, t, algo, words, count, cw_out, nerr_out, sms, as_stream(stream)));
     return QRM_OK;
 }
 
@@ -1229,7 +1232,7 @@ QRM_EXPORT qrm_status qrm_rs_decode_symbols_device(int m, int n, int k, const ui
     if (!e.empty()) return fail(QRM_INVALID_INPUT, e);
     if (count < 0) return fail(QRM_INVALID_INPUT, "negative count");
     const int t = (n - k) / 2;
-    if (t > 16) return fail(QRM_INVALID_INPUT, "symbol decoder supports t <= 16");
+    if (t > 31) return fail(QRM_INVALID_INPUT, "symbol decoder supports t <= 31");
     const RsTables* tab;
     qrm_status s = rs_tables_for(m, n, k, &tab);
     if (s != QRM_OK) return s;
@@ -1257,6 +1260,35 @@ QRM_EXPORT qrm_status qrm_rs_stress_device(int m, int n, int k, uint64_t seed, i
     QRM_LAUNCH(launch_rs_stress(tab, dm, seed, count, msg, words, nerr_true, as_stream(stream)));
     QRM_CUDA(cudaStreamSynchronize(as_stream(stream)));
     cudaFree(dm);
+    return QRM_OK;
+}
+
+QRM_EXPORT qrm_status qrm_rs_stress_symbols_device(int m, int n, int k, uint64_t seed, int64_t count,
+                                                   uint8_t* true_cw, uint8_t* recv, int8_t* nerr_true, void* stream) {
+    const std::string e = check_code(m, n, k);
+    if (!e.empty()) return fail(QRM_INVALID_INPUT, e);
+    if (m > 8) return fail(QRM_INVALID_INPUT, "symbol stress words need m <= 8");
+    const int r = n - k;
+    if (static_cast<int64_t>(k) * r > 96 * 1024) return fail(QRM_INVALID_INPUT, "parity generator exceeds 96 KiB");
+    if (count < 0) return fail(QRM_INVALID_INPUT, "negative count");
+    const RsTables* tab;
+    qrm_status s = rs_tables_for(m, n, k, &tab);
+    if (s != QRM_OK) return s;
+    // parity generator: G[j][c] = parity symbol c of rs_encode(unit message j) (encoding is GF-linear)
+    std::vector<uint8_t> gpar(static_cast<size_t>(k) * r);
+    std::vector<uint16_t> msg(k, 0);
+    for (int j = 0; j < k; ++j) {
+        msg[j] = 1;
+        const auto cw = encode_symbols(m, n, k, msg);
+        msg[j] = 0;
+        for (int c = 0; c < r; ++c) gpar[static_cast<size_t>(j) * r + c] = static_cast<uint8_t>(cw[k + c]);
+    }
+    uint8_t* dg = nullptr;
+    QRM_CUDA(cudaMalloc(&dg, std::max<size_t>(1, gpar.size())));
+    QRM_CUDA(cudaMemcpy(dg, gpar.data(), gpar.size(), cudaMemcpyHostToDevice));
+    QRM_LAUNCH(launch_rs_stress_symbols(tab, dg, k, r, seed, count, true_cw, recv, nerr_true, as_stream(stream)));
+    QRM_CUDA(cudaStreamSynchronize(as_stream(stream)));
+    cudaFree(dg);
     return QRM_OK;
 }
 

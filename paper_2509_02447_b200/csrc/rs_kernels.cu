@@ -2,6 +2,7 @@
 // and the RS stress-word generator used by the RS-only benchmark.
 #include <cuda_runtime.h>
 
+
 #include "qrm_device.cuh"
 #include "qrm_rs.cuh"
 #include "qrm_types.h"
@@ -60,62 +61,136 @@ __global__ void __launch_bounds__(256) rs_t1_packed_x4_kernel(const RsTables* __
     }
 }
 
-// One codeword per warp, packed words (n <= 32 symbols).
-template <int TMAX>
-__global__ void __launch_bounds__(256) rs_warp_packed_kernel(const RsTables* __restrict__ g,
-                                                            const uint64_t* __restrict__ words, int64_t count,
-                                                            uint64_t* __restrict__ cw_out,
+// General t, packed words (n*m <= 64). A warp owns chunks of 32 consecutive
+// words (one coalesced 8-byte load per lane, the next chunk prefetched while
+// this one is decoded). Syndromes are GF(2)-linear parities of the packed
+// word, so each lane first forms its own word's r*m syndrome bits (popc over
+// the masks); words with a nonzero syndrome are then decoded W lanes per word,
+// 32/W at a time: the segment takes the word's syndromes by shuffle, runs
+// Berlekamp-Massey, the lane-parallel Chien search over positions sl + W p and
+// Forney (seg_locate), and ORs the corrections into the word; the owning lane
+// receives the result and rechecks all n-k checks on it. Results are written
+// back with one coalesced store per lane.
+template <int W, int P, int TMAX>
+__global__ void __launch_bounds__(256) rs_seg_packed_kernel(const RsTables* __restrict__ g,
+                                                           const uint64_t* __restrict__ words, int64_t count,
+                                                           uint64_t* __restrict__ cw_out,
+                                                           int8_t* __restrict__ nerr_out) {
+    __shared__ RsSmem T;
+    rs_stage_tables(T, g, threadIdx.x, blockDim.x);
+    __syncthreads();
+    constexpr int RMAX = 2 * TMAX + 1;
+    constexpr int kPerRound = 32 / W;
+    const int lane = threadIdx.x & 31;
+    const int sl = lane & (W - 1);
+    const int seg = lane / W;
+    const int m = T.m, n = T.n, r = T.r, t = T.t, nm = T.nmask;
+    const uint32_t smask = (1u << m) - 1;
+    auto syndrome_bits = [&](uint64_t w) {
+        uint64_t sb = 0;
+        for (int b = 0; b < nm; ++b) {
+            const uint64_t x = w & T.synd_mask[b];
+            sb |= static_cast<uint64_t>(__popc(static_cast<uint32_t>(x) ^ static_cast<uint32_t>(x >> 32)) & 1) << b;
+        }
+        return sb;
+    };
+    const int64_t warp_id = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5) * 32;
+    int64_t base = warp_id * 32;
+    uint64_t wnext = base + lane < count ? __ldcs(words + base + lane) : 0ull;
+    for (; base < count; base += stride) {  // warp-uniform loop
+        const int64_t i = base + lane;
+        const bool live = i < count;
+        const uint64_t w = wnext;
+        if (base + stride + lane < count) wnext = __ldcs(words + base + stride + lane);
+        const uint64_t sb = live ? syndrome_bits(w) : 0ull;
+        uint64_t cw = w;
+        int nerr = 0;
+        uint32_t pending = __ballot_sync(0xffffffffu, sb != 0);
+        const int my_rank = __popc(pending & ((1u << lane) - 1));  // among the words needing correction
+        int round_base = 0;
+        while (pending) {  // warp-uniform: kPerRound words per round
+            uint32_t rest = pending;  // this segment's word: the seg-th set bit of pending (32: none)
+#pragma unroll
+            for (int q = 0; q < kPerRound - 1; ++q)
+                if (q < seg) rest &= rest - 1;
+            const int j = rest ? __ffs(rest) - 1 : 32;
+            const int src = j < 32 ? j : 0;
+            const uint64_t wj = __shfl_sync(0xffffffffu, w, src);
+            const uint64_t sb_src = __shfl_sync(0xffffffffu, sb, src);  // every lane shuffles (no divergent sync)
+            const uint64_t sj = j < 32 ? sb_src : 0ull;
+            uint32_t S[RMAX];
+#pragma unroll
+            for (int q = 0; q < RMAX; ++q) S[q] = q < r ? static_cast<uint32_t>(sj >> (q * m)) & smask : 0u;
+            uint32_t err[P];
+            const int changed = seg_locate<TMAX, W, P>(T, S, lane, err);
+            uint64_t part = 0;
+#pragma unroll
+            for (int q = 0; q < P; ++q) {
+                const int pos = sl + W * q;
+                if (pos < n && changed > 0) part |= static_cast<uint64_t>(err[q]) << (m * (n - 1 - pos));
+            }
+#pragma unroll
+            for (int o = W / 2; o > 0; o >>= 1) part |= __shfl_xor_sync(0xffffffffu, part, o);
+            // the owning lane takes its word's result from segment (rank - round_base)
+            const int from = (my_rank - round_base) * W;
+            const bool mine = sb != 0 && my_rank >= round_base && my_rank < round_base + kPerRound;
+            const uint64_t got_part = __shfl_sync(0xffffffffu, part, mine ? from : 0);
+            const int got_changed = __shfl_sync(0xffffffffu, changed, mine ? from : 0);
+            if (mine) {
+                const uint64_t c2 = w ^ got_part;
+                if (got_changed < 0 || got_changed > t || syndrome_bits(c2) != 0) {
+                    nerr = -1;
+                } else {
+                    nerr = got_changed;
+                    cw = c2;
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < kPerRound; ++q) pending &= pending - 1;  // drop this round's words
+            round_base += kPerRound;
+        }
+        if (live) {
+            __stcs(cw_out + i, nerr >= 0 ? cw : 0ull);
+            __stcs(reinterpret_cast<signed char*>(nerr_out) + i, static_cast<signed char>(nerr));
+        }
+    }
+}
+
+// General t, symbol bytes: one codeword per segment of W lanes (n <= 32), or
+// per warp with P symbols per lane (n <= 32 P).
+template <int TMAX, int W, int P>
+__global__ void __launch_bounds__(256) rs_seg_symbols_kernel(const RsTables* __restrict__ g,
+                                                            const uint8_t* __restrict__ recv, int64_t count,
+                                                            uint8_t* __restrict__ cw_out,
                                                             int8_t* __restrict__ nerr_out) {
     __shared__ RsSmem T;
     rs_stage_tables(T, g, threadIdx.x, blockDim.x);
     __syncthreads();
     const int lane = threadIdx.x & 31;
-    const int64_t warps = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
-    const int m = T.m, n = T.n;
-    const uint32_t smask = (1u << m) - 1;
-    for (int64_t i = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5); i < count;
-         i += warps) {
-        const uint64_t w = words[i];
-        uint32_t sym[1];
-        sym[0] = lane < n ? static_cast<uint32_t>((w >> (m * (n - 1 - lane))) & smask) : 0u;
-        const int e = rs_warp_bm<TMAX, 1>(T, sym, lane);
-        uint64_t part = (e >= 0 && lane < n) ? static_cast<uint64_t>(sym[0]) << (m * (n - 1 - lane)) : 0ull;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) part |= __shfl_xor_sync(0xffffffffu, part, o);
-        if (lane == 0) {
-            cw_out[i] = part;
-            nerr_out[i] = static_cast<int8_t>(e);
-        }
-    }
-}
-
-// One codeword per warp, symbol bytes (any n <= 255).
-template <int TMAX, int P>
-__global__ void __launch_bounds__(256) rs_warp_symbols_kernel(const RsTables* __restrict__ g,
-                                                             const uint8_t* __restrict__ recv, int64_t count,
-                                                             uint8_t* __restrict__ cw_out,
-                                                             int8_t* __restrict__ nerr_out) {
-    __shared__ RsSmem T;
-    rs_stage_tables(T, g, threadIdx.x, blockDim.x);
-    __syncthreads();
-    const int lane = threadIdx.x & 31;
+    const int sl = lane & (W - 1);
+    constexpr int kPerWarp = 32 / W;
     const int64_t warps = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
     const int n = T.n;
-    for (int64_t i = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5); i < count;
-         i += warps) {
+    for (int64_t base = (static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5)) * kPerWarp;
+         base < count; base += warps * kPerWarp) {  // warp-uniform loop
+        const int64_t i = base + lane / W;
+        const bool live = i < count;
         uint32_t sym[P];
 #pragma unroll
         for (int p = 0; p < P; ++p) {
-            const int pos = lane + 32 * p;
-            sym[p] = pos < n ? recv[i * n + pos] : 0u;
+            const int pos = sl + W * p;
+            sym[p] = (live && pos < n) ? recv[i * n + pos] : 0u;
         }
-        const int e = rs_warp_bm<TMAX, P>(T, sym, lane);
+        const int e = rs_seg_bm<TMAX, W, P>(T, sym, lane);
+        if (live) {
 #pragma unroll
-        for (int p = 0; p < P; ++p) {
-            const int pos = lane + 32 * p;
-            if (pos < n) cw_out[i * n + pos] = e >= 0 ? static_cast<uint8_t>(sym[p]) : 0;
+            for (int p = 0; p < P; ++p) {
+                const int pos = sl + W * p;
+                if (pos < n) cw_out[i * n + pos] = e >= 0 ? static_cast<uint8_t>(sym[p]) : 0;
+            }
+            if (sl == 0) nerr_out[i] = static_cast<int8_t>(e);
         }
-        if (lane == 0) nerr_out[i] = static_cast<int8_t>(e);
     }
 }
 
@@ -158,7 +233,86 @@ __global__ void rs_stress_kernel(const RsTables* __restrict__ g, const uint64_t*
     }
 }
 
-cudaError_t launch_rs_packed(const RsTables* tab, int m, int r, int t, int algo, const uint64_t* words,
+// RS stress words for symbol codes (any n): one warp per word. Message
+// symbols are counter-RNG draws; the parity symbols are GF(2^m)-linear in the
+// message (encoding is linear), parity_c = xor_j a_j * G[j][c] with G[j] the
+// parity of the j-th unit message (host rs_encode), staged in shared memory.
+// Errors as in rs_stress_kernel: e ~ U{0..t} for 90% of words and
+// U{t+1..t+2} for the other 10%, at distinct positions, each XOR (1 + below(q-1)).
+__global__ void __launch_bounds__(256) rs_stress_symbols_kernel(const RsTables* __restrict__ g,
+                                                               const uint8_t* __restrict__ gpar, uint64_t seed,
+                                                               int64_t count, uint8_t* __restrict__ true_cw,
+                                                               uint8_t* __restrict__ recv,
+                                                               int8_t* __restrict__ nerr_true) {
+    extern __shared__ uint8_t sg[];  // [k][r] parity generator
+    __shared__ RsSmem T;
+    rs_stage_tables(T, g, threadIdx.x, blockDim.x);
+    const int n = g->n, k = g->k, r = g->r, t = g->t, q1 = g->q1, m = g->m;
+    for (int i = threadIdx.x; i < k * r; i += blockDim.x) sg[i] = gpar[i];
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    const int64_t warps = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
+    for (int64_t w = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5); w < count;
+         w += warps) {
+        const uint64_t u = static_cast<uint64_t>(w);
+        uint8_t* tc = true_cw + w * n;
+        uint8_t* rc = recv + w * n;
+        for (int c0 = 0; c0 < ((r + 31) & ~31); c0 += 32) {
+            const int c = c0 + lane;
+            uint32_t par = 0;
+            for (int j = 0; j < k; ++j) {
+                const uint32_t a = static_cast<uint32_t>(rng_word(seed, 0, u * 256 + j)) & (q1 > 0 ? ((1u << m) - 1) : 0u);
+                if (c < r) par ^= gf_mul(T, a, sg[j * r + c]);
+                if (c0 == 0 && (j & 31) == lane) {
+                    tc[j] = static_cast<uint8_t>(a);
+                    rc[j] = static_cast<uint8_t>(a);
+                }
+            }
+            if (c < r) {
+                tc[k + c] = static_cast<uint8_t>(par);
+                rc[k + c] = static_cast<uint8_t>(par);
+            }
+        }
+        __syncwarp();
+        if (lane == 0) {
+            int e;
+            if (rng_below(seed, 1, u, 10) == 0) e = t + 1 + static_cast<int>(rng_below(seed, 2, u, 2));
+            else e = static_cast<int>(rng_below(seed, 2, u, static_cast<uint64_t>(t + 1)));
+            if (e > n) e = n;
+            uint32_t used[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+            uint64_t ctr = 0;
+            for (int j = 0; j < e; ++j) {
+                int pos;
+                do {
+                    pos = static_cast<int>(rng_below(seed, 3 + u * 2, ctr++, static_cast<uint64_t>(n)));
+                } while ((used[pos >> 5] >> (pos & 31)) & 1);
+                used[pos >> 5] |= 1u << (pos & 31);
+                rc[pos] ^= static_cast<uint8_t>(1 + rng_below(seed, 4 + u * 2, static_cast<uint64_t>(j), static_cast<uint64_t>(q1)));
+            }
+            nerr_true[w] = static_cast<int8_t>(e);
+        }
+        __syncwarp();
+    }
+}
+
+cudaError_t launch_rs_stress_symbols(const RsTables* tab, const uint8_t* gpar, int k, int r, uint64_t seed,
+                                     int64_t count, uint8_t* true_cw, uint8_t* recv, int8_t* nerr_true,
+                                     cudaStream_t st) {
+    if (count <= 0) return cudaSuccess;
+    int64_t blocks = (count + 7) / 8;
+    if (blocks > 148 * 8) blocks = 148 * 8;
+    const size_t smem = static_cast<size_t>(k) * r;
+    if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(rs_stress_symbols_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             static_cast<int>(smem));
+        if (e != cudaSuccess) return e;
+    }
+    rs_stress_symbols_kernel<<<static_cast<unsigned>(blocks), 256, smem, st>>>(tab, gpar, seed, count, true_cw, recv,
+                                                                               nerr_true);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_rs_packed(const RsTables* tab, int m, int n, int r, int t, int algo, const uint64_t* words,
                              int64_t count, uint64_t* cw, int8_t* nerr, int sm_count, cudaStream_t st) {
     if (count <= 0) return cudaSuccess;
     const int sms = sm_count > 0 ? sm_count : 148;
@@ -188,14 +342,20 @@ cudaError_t launch_rs_packed(const RsTables* tab, int m, int r, int t, int algo,
                                                                                nerr + done);
         }
     } else {
-        int64_t blocks = (count + 7) / 8;
+        // 4 lanes per word (8 words per round): measured 11.3 G words/s on gf16-15-12 stress words
+        // against 9.5 (8 lanes) and 6.7 (16 lanes) — the segment-uniform work (BM) amortises over
+        // more words. Packed words have n <= 15 (m = 4) or n <= 8 (m = 8): 4 or 2 positions per lane.
+        int64_t blocks = (count + 255) / 256;
         const int64_t cap = static_cast<int64_t>(sms) * 16;
         if (blocks > cap) blocks = cap;
         const unsigned b = static_cast<unsigned>(blocks);
-        if (t <= 1) rs_warp_packed_kernel<1><<<b, 256, 0, st>>>(tab, words, count, cw, nerr);
-        else if (t <= 2) rs_warp_packed_kernel<2><<<b, 256, 0, st>>>(tab, words, count, cw, nerr);
-        else if (t <= 4) rs_warp_packed_kernel<4><<<b, 256, 0, st>>>(tab, words, count, cw, nerr);
-        else rs_warp_packed_kernel<8><<<b, 256, 0, st>>>(tab, words, count, cw, nerr);
+        if (n <= 8 && t <= 1) rs_seg_packed_kernel<4, 2, 1><<<b, 256, 0, st>>>(tab, words, count, cw, nerr);
+        else if (n <= 8 && t <= 2) rs_seg_packed_kernel<4, 2, 2><<<b, 256, 0, st>>>(tab, words, count, cw, nerr);
+        else if (n <= 8) rs_seg_packed_kernel<4, 2, 4><<<b, 256, 0, st>>>(tab, words, count, cw, nerr);
+        else if (t <= 1) rs_seg_packed_kernel<4, 4, 1><<<b, 256, 0, st>>>(tab, words, count, cw, nerr);
+        else if (t <= 2) rs_seg_packed_kernel<4, 4, 2><<<b, 256, 0, st>>>(tab, words, count, cw, nerr);
+        else if (t <= 4) rs_seg_packed_kernel<4, 4, 4><<<b, 256, 0, st>>>(tab, words, count, cw, nerr);
+        else rs_seg_packed_kernel<4, 4, 8><<<b, 256, 0, st>>>(tab, words, count, cw, nerr);
     }
     return cudaGetLastError();
 }
@@ -204,21 +364,30 @@ cudaError_t launch_rs_symbols(const RsTables* tab, int n, int t, const uint8_t* 
                               int8_t* nerr, int sm_count, cudaStream_t st) {
     if (count <= 0) return cudaSuccess;
     const int sms = sm_count > 0 ? sm_count : 148;
-    int64_t blocks = (count + 7) / 8;
+    // narrow segments for short codes (W = 4 or 8 lanes, 4 positions each), a warp per long codeword
+    const int W = n <= 16 ? 4 : n <= 32 ? 8 : 32;
+    int64_t blocks = (count * W + 255) / 256;
     const int64_t cap = static_cast<int64_t>(sms) * 16;
     if (blocks > cap) blocks = cap;
     const unsigned b = static_cast<unsigned>(blocks);
-    if (n <= 32) {
-        if (t <= 1) rs_warp_symbols_kernel<1, 1><<<b, 256, 0, st>>>(tab, recv, count, cw, nerr);
-        else if (t <= 2) rs_warp_symbols_kernel<2, 1><<<b, 256, 0, st>>>(tab, recv, count, cw, nerr);
-        else if (t <= 4) rs_warp_symbols_kernel<4, 1><<<b, 256, 0, st>>>(tab, recv, count, cw, nerr);
-        else if (t <= 8) rs_warp_symbols_kernel<8, 1><<<b, 256, 0, st>>>(tab, recv, count, cw, nerr);
-        else rs_warp_symbols_kernel<16, 1><<<b, 256, 0, st>>>(tab, recv, count, cw, nerr);
-    } else {
-        if (t <= 2) rs_warp_symbols_kernel<2, 8><<<b, 256, 0, st>>>(tab, recv, count, cw, nerr);
-        else if (t <= 4) rs_warp_symbols_kernel<4, 8><<<b, 256, 0, st>>>(tab, recv, count, cw, nerr);
-        else if (t <= 8) rs_warp_symbols_kernel<8, 8><<<b, 256, 0, st>>>(tab, recv, count, cw, nerr);
-        else rs_warp_symbols_kernel<16, 8><<<b, 256, 0, st>>>(tab, recv, count, cw, nerr);
+    // t <= (n - 1) / 2: n <= 16 -> t <= 7, n <= 32 -> t <= 15
+    if (n <= 16) {
+        if (t <= 1) rs_seg_symbols_kernel<1, 4, 4><<<b, 256, 0, st>>>(tab, recv, count, cw, nerr);
+        else if (t <= 2) rs_seg_symbols_kernel<2, 4, 4><<<b, 256, 0, st>>>(tab, recv, count, cw, nerr);
+        else if (t <= 4) rs_seg_symbols_kernel<4, 4, 4><<<b, 256, 0, st>>>(tab, recv, count, cw, nerr);
+        else rs_seg_symbols_kernel<8, 4, 4><<<b, 256, 0, st>>>(tab, recv, count, cw, nerr);
+    } else if (n <= 32) {
+        if (t <= 2) rs_seg_symbols_kernel<2, 8, 4><<<b, 256, 0, st>>>(tab, recv, count, cw, nerr);
+        else if (t <= 4) rs_seg_symbols_kernel<4, 8, 4><<<b, 256, 0, st>>>(tab, recv, count, cw, nerr);
+        else if (t <= 8) rs_seg_symbols_kernel<8, 8, 4><<<b, 256, 0, st>>>(tab, recv, count, cw, nerr);
+        else rs_seg_symbols_kernel<16, 8, 4><<<b, 256, 0, st>>>(tab, recv, count, cw, nerr);
+    }
+    if (n > 32) {
+        if (t <= 2) rs_seg_symbols_kernel<2, 32, 8><<<b, 256, 0, st>>>(tab, recv, count, cw, nerr);
+        else if (t <= 4) rs_seg_symbols_kernel<4, 32, 8><<<b, 256, 0, st>>>(tab, recv, count, cw, nerr);
+        else if (t <= 8) rs_seg_symbols_kernel<8, 32, 8><<<b, 256, 0, st>>>(tab, recv, count, cw, nerr);
+        else if (t <= 16) rs_seg_symbols_kernel<16, 32, 8><<<b, 256, 0, st>>>(tab, recv, count, cw, nerr);
+        else rs_seg_symbols_kernel<31, 32, 8><<<b, 256, 0, st>>>(tab, recv, count, cw, nerr);
     }
     return cudaGetLastError();
 }

@@ -179,3 +179,51 @@ def test_stress_10m_bit_exact_vs_reference(qrm, cuda, ref):
         ne_g = ne.cpu().numpy()
         assert np.array_equal(ne_g, ne_r), algo
         assert np.array_equal(cw.cpu().numpy().view(np.uint64)[ok], cw_r[ok]), algo
+
+
+@pytest.mark.parametrize("mnk", [(4, 15, 9), (4, 15, 7), (4, 15, 5), (4, 15, 1), (8, 8, 4), (8, 8, 2), (4, 4, 2)])
+def test_segmented_packed_general_t_matches_oracle(qrm, cuda, orc, mnk):
+    """Segmented warp decoder (W lanes per word, ballot syndromes) on packed
+    codes with t >= 2, every output against the C restatement of bw_decode."""
+    m, n, k = mnk
+    code = qrm.CodeParams.make(m, n, k)
+    rng = np.random.default_rng(m * 100 + n + k)
+    N = 20000
+    msgs = _random_msgs(rng, N, code.message_bits())
+    cws = _encode_all(qrm, code, msgs)
+    nerr = rng.integers(0, code.t + 3, size=N)
+    nerr = np.minimum(nerr, n)
+    words = _corrupt(rng, cws, m, n, nerr)
+    words = np.concatenate([words, _random_msgs(rng, 3001, code.codeword_bits())])  # ragged tail
+    cw_g, ne_g = _gpu_decode(qrm, cuda, code, words, 2)
+    cw_o, ne_o = orc.bw_decode_packed(m, n, k, words)
+    assert np.array_equal(ne_g, ne_o)
+    ok = ne_o >= 0
+    assert np.array_equal(cw_g[ok], cw_o[ok])
+    small = np.arange(N)[nerr <= code.t]
+    assert np.array_equal(cw_g[small], cws[small])
+
+
+@pytest.mark.parametrize("mnk,count", [((8, 12, 8), 4000), ((8, 30, 20), 1000), ((8, 255, 223), 96), ((8, 8, 6), 4000), ((8, 255, 200), 48), ((8, 100, 40), 48), ((4, 15, 3), 4000)])
+def test_symbol_stress_words_match_reference(qrm, cuda, ref, mnk, count):
+    """Device symbol stress words (the GF(2^8) RS bench inputs): the codewords are
+    the reference's rs_encode of their message prefix, and the GPU decoder
+    equals the compiled reference's bw_decode on every received word."""
+    m, n, k = mnk
+    code = qrm.CodeParams.make(m, n, k)
+    true_cw, recv, ne_true = qrm.rs_stress_symbols(code, 77, count)
+    cw_g, ne_g = qrm.bw_decode_symbols(code, recv)
+    cuda.cuda.synchronize()
+    true_cw, recv, ne_true = true_cw.cpu().numpy(), recv.cpu().numpy(), ne_true.cpu().numpy()
+    cw_g, ne_g = cw_g.cpu().numpy(), ne_g.cpu().numpy()
+    for i in range(0, count, max(1, count // 16)):  # encoder: systematic prefix -> reference rs_encode
+        bits = np.array([(int(v) >> (m - 1 - b)) & 1 for v in true_cw[i, :k] for b in range(m)], np.uint8)
+        cwb = ref.rs_encode(m, n, k, bits)
+        assert np.array_equal(true_cw[i], [oracle.bits_to_word(cwb[m * j:m * j + m]) for j in range(n)])
+    assert (ne_true > code.t).any() and (ne_true == 0).any()
+    cw_r, ne_r, _ = ref.bw_decode_symbols_mt(m, n, k, recv, threads=16)
+    assert np.array_equal(ne_g, ne_r)
+    ok = ne_r >= 0
+    assert np.array_equal(cw_g[ok], cw_r[ok])
+    small = ne_true <= code.t
+    assert np.array_equal(cw_g[small], true_cw[small]) and np.array_equal(ne_g[small], ne_true[small])
