@@ -340,10 +340,15 @@ QRM_EXPORT qrm_status qrm_extract_float_host(uint64_t key_seed, int n_bits, int 
  * distance t or failure. nerr_out[i] = errors_corrected, or -1 for a decode
  * failure (nullopt). */
 /* Packed words (n*m <= 64). algo 0: auto; 1: thread-per-codeword syndrome
- * decoder (t = 1 codes); 2: warp-per-codeword Berlekamp-Massey/Chien/Forney. */
+ * decoder (t = 1 codes); 2: segmented-warp Berlekamp-Massey/Chien/Forney (4
+ * lanes per codeword, any t <= 8); 3: algo 2 behind the device codebook (the
+ * CorrectionCache analog, detect.cpp:86-128: a per-(device, code) memo of
+ * decoded words, n*m < 64; results are identical with or without it). */
 QRM_EXPORT qrm_status qrm_rs_decode_packed_device(int m, int n, int k, const uint64_t* words, int64_t count,
                                                   uint64_t* cw_out, int8_t* nerr_out, int algo, void* stream);
 /* Symbol arrays (any n <= 2^m - 1, m in {4, 8}): count*n bytes in/out. */
+/* Empty the device codebook of code (m, n, k) on the current device. */
+QRM_EXPORT qrm_status qrm_rs_codebook_clear(int m, int n, int k, void* stream);
 QRM_EXPORT qrm_status qrm_rs_decode_symbols_device(int m, int n, int k, const uint8_t* recv, int64_t count,
                                                    uint8_t* cw_out, int8_t* nerr_out, void* stream);
 /* RS stress words (SURVEY 8d recipe) on the device: per word a random message,

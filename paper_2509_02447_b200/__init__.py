@@ -29,7 +29,7 @@ ABI_SYMBOLS = (
     "qrm_last_error", "qrm_abi_version", "qrm_device_count", "qrm_ctx_create", "qrm_ctx_destroy", "qrm_ctx_info",
     "qrm_ctx_set_extractor", "qrm_ppm_read", "qrm_ppm_write", "qrm_ppm_read_batch", "qrm_records_json", "qrm_cache_hits", "qrm_attack_device", "qrm_warmup_profile_mode", "qrm_extract_tiles_device", "qrm_detect_host_multi", "qrm_detect_host_lpt", "qrm_ctx_set_transfer_split",
     "qrm_detect_device", "qrm_detect_host", "qrm_detect_ragged", "qrm_extract_device", "qrm_preprocess_host",
-    "qrm_rs_decode_packed_device", "qrm_rs_decode_symbols_device", "qrm_rs_stress_device", "qrm_rs_stress_symbols_device", "qrm_rs_encode_packed",
+    "qrm_rs_decode_packed_device", "qrm_rs_decode_symbols_device", "qrm_rs_stress_device", "qrm_rs_stress_symbols_device", "qrm_rs_codebook_clear", "qrm_rs_encode_packed",
     "qrm_verify_threshold", "qrm_make_corpus_device", "qrm_patterns_device", "qrm_allocate_streams",
     "qrm_lpt_schedule", "qrm_warmup_profile", "qrm_ctx_set_plan", "qrm_kernel_launch_count",
     "qrm_probe_decode_kernel", "qrm_resample_host", "qrm_extract_float_host", "qrm_hidden_detect_device",
@@ -135,6 +135,7 @@ def lib() -> C.CDLL:
         L.qrm_rs_decode_symbols_device.argtypes = [i32, i32, i32, vp, i64, vp, vp, vp]
         L.qrm_rs_stress_device.argtypes = [i32, i32, i32, u64, i64, vp, vp, vp, vp]
         L.qrm_rs_stress_symbols_device.argtypes = [i32, i32, i32, u64, i64, vp, vp, vp, vp]
+        L.qrm_rs_codebook_clear.argtypes = [i32, i32, i32, vp]
         L.qrm_rs_encode_packed.argtypes = [i32, i32, i32, u64, C.POINTER(u64)]
         L.qrm_verify_threshold.argtypes = [i32, C.c_double, C.POINTER(i32)]
         L.qrm_make_corpus_device.argtypes = [C.POINTER(_Config), u64, i64, i32, i32, i32, vp, vp]
@@ -311,6 +312,11 @@ def bw_decode_symbols_into(code: CodeParams, recv, cw_out, nerr_out, stream=None
     _check(lib().qrm_rs_decode_symbols_device(code.m, code.n, code.k, _ptr(recv), recv.shape[0], _ptr(cw_out),
                                               _ptr(nerr_out), _stream(stream)))
     return cw_out, nerr_out
+
+
+def rs_codebook_clear(code: CodeParams, stream=None):
+    """Empty the device codebook (algo 3 of bw_decode_packed) for `code`."""
+    _check(lib().qrm_rs_codebook_clear(code.m, code.n, code.k, _stream(stream)))
 
 
 def bw_decode_packed(code: CodeParams, words, cw_out=None, nerr_out=None, algo: int = 0, stream=None):

@@ -49,7 +49,8 @@ cudaError_t launch_tile_bf16(const CUtensorMap& tmap, const TileBf16Params& p, i
 cudaError_t launch_attack_jpeg(const AttackParams& p, cudaStream_t st);
 cudaError_t launch_attack_resample(const AttackParams& p, cudaStream_t st);
 cudaError_t launch_rs_packed(const RsTables* tab, int m, int n, int r, int t, int algo, const uint64_t* words,
-                             int64_t count, uint64_t* cw, int8_t* nerr, int sm_count, cudaStream_t st);
+                             int64_t count, uint64_t* cw, int8_t* nerr, int sm_count, cudaStream_t st,
+                             CodebookTable cache);
 cudaError_t launch_rs_symbols(const RsTables* tab, int n, int t, const uint8_t* recv, int64_t count, uint8_t* cw,
                               int8_t* nerr, int sm_count, cudaStream_t st);
 cudaError_t launch_rs_stress_symbols(const RsTables* tab, const uint8_t* gpar, int k, int r, uint64_t seed,
@@ -1206,6 +1207,28 @@ QRM_EXPORT qrm_status qrm_preprocess_host(const uint8_t* image, int w, int h, fl
     return QRM_OK;
 }
 
+// Device codebooks (row f1), one per (device, code), created on first use:
+// 2^22 slots (64 MiB of keys + values, 4 MiB of error counts), keys all-ones.
+static std::mutex g_codebook_mu;
+static std::map<std::tuple<int, int, int, int>, CodebookTable> g_codebooks;
+constexpr uint64_t kCodebookSlots = 1ull << 22;
+
+static qrm_status codebook_for(int dev, int m, int n, int k, cudaStream_t st, CodebookTable* out) {
+    std::lock_guard<std::mutex> g(g_codebook_mu);
+    auto key = std::make_tuple(dev, m, n, k);
+    auto it = g_codebooks.find(key);
+    if (it == g_codebooks.end()) {
+        CodebookTable c{nullptr, nullptr, nullptr, kCodebookSlots - 1};
+        QRM_CUDA(cudaMalloc(&c.keys, sizeof(uint64_t) * kCodebookSlots));
+        QRM_CUDA(cudaMalloc(&c.vals, sizeof(uint64_t) * kCodebookSlots));
+        QRM_CUDA(cudaMalloc(&c.nerr, kCodebookSlots));
+        QRM_CUDA(cudaMemsetAsync(c.keys, 0xFF, sizeof(uint64_t) * kCodebookSlots, st));
+        it = g_codebooks.emplace(key, c).first;
+    }
+    *out = it->second;
+    return QRM_OK;
+}
+
 QRM_EXPORT qrm_status qrm_rs_decode_packed_device(int m, int n, int k, const uint64_t* words, int64_t count,
                                                   uint64_t* cw_out, int8_t* nerr_out, int algo, void* stream) {
     const std::string e = check_code(m, n, k);
@@ -1214,7 +1237,9 @@ QRM_EXPORT qrm_status qrm_rs_decode_packed_device(int m, int n, int k, const uin
     if (count < 0) return fail(QRM_INVALID_INPUT, "negative count");
     const int t = (n - k) / 2;
     if (algo == 0) algo = (t == 1 && n - k <= 3) ? 1 : 2;
+    if (algo < 1 || algo > 3) return fail(QRM_INVALID_INPUT, "algo must be 0 (auto), 1, 2 or 3");
     if (algo == 1 && !(t == 1 && n - k <= 3)) return fail(QRM_INVALID_INPUT, "thread decoder needs t = 1");
+    if (algo == 3 && n * m >= 64) return fail(QRM_INVALID_INPUT, "the device codebook needs n*m < 64");
     if (t > 8) return fail(QRM_INVALID_INPUT, "packed warp decoder supports t <= 8");
     const RsTables* tab;
     qrm_status s = rs_tables_for(m, n, k, &tab);
@@ -1222,7 +1247,25 @@ QRM_EXPORT qrm_status qrm_rs_decode_packed_device(int m, int n, int k, const uin
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    QRM_LAUNCH(launch_rs_packed(tab, m, n, n - k, t, algo, words, count, cw_out, nerr_out, sms, as_stream(stream)));
+    CodebookTable cache{nullptr, nullptr, nullptr, 0};
+    if (algo == 3) {
+        s = codebook_for(dev, m, n, k, as_stream(stream), &cache);
+        if (s != QRM_OK) return s;
+    }
+    QRM_LAUNCH(launch_rs_packed(tab, m, n, n - k, t, algo == 3 ? 2 : algo, words, count, cw_out, nerr_out, sms,
+                                as_stream(stream), cache));
+    return QRM_OK;
+}
+
+QRM_EXPORT qrm_status qrm_rs_codebook_clear(int m, int n, int k, void* stream) {
+    const std::string e = check_code(m, n, k);
+    if (!e.empty()) return fail(QRM_INVALID_INPUT, e);
+    int dev = 0;
+    cudaGetDevice(&dev);
+    CodebookTable cache{nullptr, nullptr, nullptr, 0};
+    qrm_status s = codebook_for(dev, m, n, k, as_stream(stream), &cache);
+    if (s != QRM_OK) return s;
+    QRM_CUDA(cudaMemsetAsync(cache.keys, 0xFF, sizeof(uint64_t) * (cache.mask + 1), as_stream(stream)));
     return QRM_OK;
 }
 

@@ -24,6 +24,18 @@ struct alignas(16) RsTables {
     uint64_t synd_mask[64];     // packed-word syndrome bits: S_j bit e = parity(word & synd_mask[j*m+e])
 };
 
+// Device codebook (row f1): open-addressing memo word -> (codeword, errors)
+// for the general-t packed decoder. keys[i] == kCodebookEmpty: free slot.
+constexpr uint64_t kCodebookEmpty = ~0ull;     // never a packed word (n*m < 64 required)
+constexpr uint64_t kCodebookBusy = ~0ull - 1;  // claimed, value being written
+constexpr int kCodebookProbes = 8;
+struct CodebookTable {
+    uint64_t* keys;  // nullptr: no table
+    uint64_t* vals;
+    int8_t* nerr;
+    uint64_t mask;   // slots - 1 (power of two)
+};
+
 // One pending detection (tie resolution and/or general-t RS correction).
 struct PendingEntry {
     int64_t image;

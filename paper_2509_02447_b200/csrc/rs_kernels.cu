@@ -71,11 +71,18 @@ __global__ void __launch_bounds__(256) rs_t1_packed_x4_kernel(const RsTables* __
 // Forney (seg_locate), and ORs the corrections into the word; the owning lane
 // receives the result and rechecks all n-k checks on it. Results are written
 // back with one coalesced store per lane.
-template <int W, int P, int TMAX>
+//
+// With a CodebookTable (row f1: the reference's CorrectionCache, detect.cpp:
+// 86-128, as a device memo) each lane first probes the table for its word; hits
+// skip the decode, and decoded words are inserted (slot claimed by CAS, value
+// written, then the key published behind a fence, so a reader that sees the
+// key sees the value). The memo is transparent: a decode is a pure function
+// of the word.
+template <int W, int P, int TMAX, bool CACHED>
 __global__ void __launch_bounds__(256) rs_seg_packed_kernel(const RsTables* __restrict__ g,
                                                            const uint64_t* __restrict__ words, int64_t count,
                                                            uint64_t* __restrict__ cw_out,
-                                                           int8_t* __restrict__ nerr_out) {
+                                                           int8_t* __restrict__ nerr_out, CodebookTable cache) {
     __shared__ RsSmem T;
     rs_stage_tables(T, g, threadIdx.x, blockDim.x);
     __syncthreads();
@@ -103,9 +110,29 @@ __global__ void __launch_bounds__(256) rs_seg_packed_kernel(const RsTables* __re
         const bool live = i < count;
         const uint64_t w = wnext;
         if (base + stride + lane < count) wnext = __ldcs(words + base + stride + lane);
-        const uint64_t sb = live ? syndrome_bits(w) : 0ull;
         uint64_t cw = w;
         int nerr = 0;
+        bool hit = false;
+        uint64_t slot0 = 0;
+        if constexpr (CACHED) {
+            if (live) {
+                slot0 = mix64(w) & cache.mask;
+#pragma unroll 1
+                for (int pr = 0; pr < kCodebookProbes; ++pr) {
+                    const uint64_t sidx = (slot0 + pr) & cache.mask;
+                    const uint64_t key = *reinterpret_cast<volatile const uint64_t*>(cache.keys + sidx);
+                    if (key == w) {
+                        __threadfence();  // acquire: the value was published before the key
+                        cw = cache.vals[sidx];
+                        nerr = cache.nerr[sidx];
+                        hit = true;
+                        break;
+                    }
+                    if (key == kCodebookEmpty) break;
+                }
+            }
+        }
+        const uint64_t sb = (live && !hit) ? syndrome_bits(w) : 0ull;
         uint32_t pending = __ballot_sync(0xffffffffu, sb != 0);
         const int my_rank = __popc(pending & ((1u << lane) - 1));  // among the words needing correction
         int round_base = 0;
@@ -149,6 +176,24 @@ __global__ void __launch_bounds__(256) rs_seg_packed_kernel(const RsTables* __re
 #pragma unroll
             for (int q = 0; q < kPerRound; ++q) pending &= pending - 1;  // drop this round's words
             round_base += kPerRound;
+        }
+        if constexpr (CACHED) {
+            if (live && !hit && sb != 0) {  // memoise decoded (and failed) words
+#pragma unroll 1
+                for (int pr = 0; pr < kCodebookProbes; ++pr) {
+                    const uint64_t sidx = (slot0 + pr) & cache.mask;
+                    const unsigned long long old = atomicCAS(reinterpret_cast<unsigned long long*>(cache.keys + sidx),
+                                                             kCodebookEmpty, kCodebookBusy);
+                    if (old == kCodebookEmpty) {
+                        cache.vals[sidx] = cw;
+                        cache.nerr[sidx] = static_cast<int8_t>(nerr);
+                        __threadfence();  // release: value before key
+                        *reinterpret_cast<volatile uint64_t*>(cache.keys + sidx) = w;
+                        break;
+                    }
+                    if (old == w) break;  // another lane inserted it
+                }
+            }
         }
         if (live) {
             __stcs(cw_out + i, nerr >= 0 ? cw : 0ull);
@@ -313,7 +358,8 @@ cudaError_t launch_rs_stress_symbols(const RsTables* tab, const uint8_t* gpar, i
 }
 
 cudaError_t launch_rs_packed(const RsTables* tab, int m, int n, int r, int t, int algo, const uint64_t* words,
-                             int64_t count, uint64_t* cw, int8_t* nerr, int sm_count, cudaStream_t st) {
+                             int64_t count, uint64_t* cw, int8_t* nerr, int sm_count, cudaStream_t st,
+                             CodebookTable cache) {
     if (count <= 0) return cudaSuccess;
     const int sms = sm_count > 0 ? sm_count : 148;
     if (algo == 1) {
@@ -349,13 +395,17 @@ cudaError_t launch_rs_packed(const RsTables* tab, int m, int n, int r, int t, in
         const int64_t cap = static_cast<int64_t>(sms) * 16;
         if (blocks > cap) blocks = cap;
         const unsigned b = static_cast<unsigned>(blocks);
-        if (n <= 8 && t <= 1) rs_seg_packed_kernel<4, 2, 1><<<b, 256, 0, st>>>(tab, words, count, cw, nerr);
-        else if (n <= 8 && t <= 2) rs_seg_packed_kernel<4, 2, 2><<<b, 256, 0, st>>>(tab, words, count, cw, nerr);
-        else if (n <= 8) rs_seg_packed_kernel<4, 2, 4><<<b, 256, 0, st>>>(tab, words, count, cw, nerr);
-        else if (t <= 1) rs_seg_packed_kernel<4, 4, 1><<<b, 256, 0, st>>>(tab, words, count, cw, nerr);
-        else if (t <= 2) rs_seg_packed_kernel<4, 4, 2><<<b, 256, 0, st>>>(tab, words, count, cw, nerr);
-        else if (t <= 4) rs_seg_packed_kernel<4, 4, 4><<<b, 256, 0, st>>>(tab, words, count, cw, nerr);
-        else rs_seg_packed_kernel<4, 4, 8><<<b, 256, 0, st>>>(tab, words, count, cw, nerr);
+#define QRM_SEGP(P, TM)                                                                                       \
+    (cache.keys ? (rs_seg_packed_kernel<4, P, TM, true><<<b, 256, 0, st>>>(tab, words, count, cw, nerr, cache), 0) \
+                : (rs_seg_packed_kernel<4, P, TM, false><<<b, 256, 0, st>>>(tab, words, count, cw, nerr, cache), 0))
+        if (n <= 8 && t <= 1) QRM_SEGP(2, 1);
+        else if (n <= 8 && t <= 2) QRM_SEGP(2, 2);
+        else if (n <= 8) QRM_SEGP(2, 4);
+        else if (t <= 1) QRM_SEGP(4, 1);
+        else if (t <= 2) QRM_SEGP(4, 2);
+        else if (t <= 4) QRM_SEGP(4, 4);
+        else QRM_SEGP(4, 8);
+#undef QRM_SEGP
     }
     return cudaGetLastError();
 }

@@ -227,3 +227,23 @@ def test_symbol_stress_words_match_reference(qrm, cuda, ref, mnk, count):
     assert np.array_equal(cw_g[ok], cw_r[ok])
     small = ne_true <= code.t
     assert np.array_equal(cw_g[small], true_cw[small]) and np.array_equal(ne_g[small], ne_true[small])
+
+
+@pytest.mark.parametrize("mnk", [(4, 15, 12), (4, 15, 11), (4, 15, 7), (8, 7, 5)])
+def test_codebook_is_transparent(qrm, cuda, orc, mnk):
+    """Device codebook (algo 3, the CorrectionCache analog): on a stream with many
+    repeats, cold and warm passes give exactly the oracle's outputs."""
+    m, n, k = mnk
+    code = qrm.CodeParams.make(m, n, k)
+    rng = np.random.default_rng(n + k)
+    uniq = np.concatenate([_corrupt(rng, _encode_all(qrm, code, _random_msgs(rng, 3000, code.message_bits())), m, n,
+                                    rng.integers(0, code.t + 3, size=3000)),
+                           _random_msgs(rng, 1000, code.codeword_bits())])
+    words = uniq[rng.integers(0, uniq.size, size=50_000)]
+    cw_o, ne_o = orc.bw_decode_packed(m, n, k, words)
+    qrm.rs_codebook_clear(code)
+    for _ in range(2):  # cold (inserting, concurrent repeats), then warm (hits)
+        cw_g, ne_g = _gpu_decode(qrm, cuda, code, words, 3)
+        assert np.array_equal(ne_g, ne_o)
+        ok = ne_o >= 0
+        assert np.array_equal(cw_g[ok], cw_o[ok])
