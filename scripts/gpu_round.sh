@@ -12,4 +12,5 @@ ncu --set full --clock-control none --import-source on -k regex:conv64 -s 7 -c 1
 ncu --set full --clock-control none --import-source on -k regex:conv0 -s 2 -c 1 -o gpurun_out/conv0 python scripts/bench_hidden.py 1024 > /dev/null 2>&1
 ncu --set full --clock-control none --import-source on -k regex:fetch_windows -s 4 -c 1 -o gpurun_out/fetch python scripts/e2e_modes.py > /dev/null 2>&1
 ncu --set full --clock-control none --import-source on -k regex:rs_t1_packed -s 3 -c 1 -o gpurun_out/rs_t1 python scripts/rs_time.py > /dev/null 2>&1
-tail -3 gpurun_out/tests.log; tail -1 gpurun_out/smoke.log; tail -2 gpurun_out/bench.err; cat gpurun_out/bench.json gpurun_out/bench_ref.json; ls gpurun_out
+bash scripts/sanitize.sh > /dev/null 2>&1
+tail -3 gpurun_out/tests.log; cat gpurun_out/sanitize_summary.txt; tail -1 gpurun_out/smoke.log; tail -2 gpurun_out/bench.err; cat gpurun_out/bench.json gpurun_out/bench_ref.json; ls gpurun_out
