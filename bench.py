@@ -275,6 +275,11 @@ def config512_submetric(q, ctx, cfg, world, rank, max_over_ranks, warmup, batch=
     t, m = ctx.warmup_profile(iters=5, b0=16, mode=0, ptr=host.data_ptr(), shape=(pool_n, 512, 512))
     free = float(torch.cuda.mem_get_info()[0])
     plan = q.allocate_streams(t, m, 16.0, batch, 16, free, 0.0, 2)
+    # GPU-aware Algorithm 1 (extension): measured per-stage saturation on 1/2/4
+    # concurrent streams caps each stage's speedup (a PCIe-bound transfer gains
+    # nothing from more streams)
+    ts, ms_, sat = ctx.warmup_saturation(iters=5, b0=256, ptr=host.data_ptr(), shape=(pool_n, 512, 512))
+    plan_gpu = q.allocate_streams_sat(ts, ms_, sat, 256.0, batch, 16, free, 0.0, 2)
     recs_pin = torch.empty((pool_n, q.RECORD_DTYPE.itemsize), dtype=torch.uint8, pin_memory=True)
     recs = recs_pin.numpy().view(q.RECORD_DTYPE).reshape(-1)
     calls = batch // pool_n
@@ -287,8 +292,11 @@ def config512_submetric(q, ctx, cfg, world, rank, max_over_ranks, warmup, batch=
 
     out = {"workload": "configs[2]: 512x512 RGB, batch 16384 (8 calls x 2048 over a pinned pool), one 64x64 tile "
                        "per image after the centre crop, mode 0 transfer",
-           "warmup_profile_ms_per_16": [float(x) for x in t], "warmup_bytes_per_image": [float(x) for x in m]}
+           "warmup_profile_ms_per_16": [float(x) for x in t], "warmup_bytes_per_image": [float(x) for x in m],
+           "saturation_warmup": {"b0": 256, "ms_per_b0_one_stream": [float(x) for x in ts],
+                                 "best_speedup_on_1_2_4_streams": [float(x) for x in sat]}}
     for name, pl in (("alg1", (plan.streams, [max(1, min(pool_n, x)) for x in plan.minibatch])),
+                     ("alg1_gpu_aware", (plan_gpu.streams, [max(1, min(pool_n, x)) for x in plan_gpu.minibatch])),
                      ("baseline_111", ([1, 1, 1], [pool_n] * 3))):
         run(pl, max(1, warmup // 3))
         torch.cuda.synchronize()

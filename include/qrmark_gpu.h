@@ -382,6 +382,14 @@ QRM_EXPORT qrm_status qrm_allocate_streams(int stages, const double* time, const
                                            int global_batch, int stream_budget, double m_cap, double epsilon,
                                            int stall_cap, int* streams_out, int* minibatch_out,
                                            double* bottleneck_out);
+/* Algorithm 1 with a GPU-aware stage model (extension; not in the reference):
+ * TIME(k, s, m) = t[k] (m / b0) / min(s, sat[k]), sat[k] the measured speedup
+ * of stage k on concurrent streams (qrm_warmup_saturation). With every sat[k]
+ * >= stream_budget this is qrm_allocate_streams. */
+QRM_EXPORT qrm_status qrm_allocate_streams_sat(int stages, const double* time, const double* memory,
+                                               const double* sat, double b0, int global_batch, int stream_budget,
+                                               double m_cap, double epsilon, int stall_cap, int* streams_out,
+                                               int* minibatch_out, double* bottleneck_out);
 /* lpt_schedule (sched.cpp:177-235): Algorithm 2. Pieces are returned stream
  * by stream in placement order. */
 QRM_EXPORT qrm_status qrm_lpt_schedule(int ntasks, const int* ids, const double* latency, const double* memory,
@@ -396,6 +404,13 @@ QRM_EXPORT qrm_status qrm_lpt_schedule(int ntasks, const int* ids, const double*
 QRM_EXPORT qrm_status qrm_warmup_profile(qrm_ctx* ctx, const uint8_t* images, int64_t count, int w, int h,
                                          int64_t image_stride, int warmup_iters, int b0, double* time,
                                          double* memory);
+/* GPU-aware warm-up (extension): the mode-0 stages (window fetch, decode,
+ * record D2H) each on 1, 2 and 4 concurrent streams of b0 images (host images,
+ * count >= 4 b0). time[3] = ms per b0 images on one stream, memory[3] bytes
+ * per image, sat[3] = best speedup s T(1) / T(s) (1 = no gain from streams). */
+QRM_EXPORT qrm_status qrm_warmup_saturation(qrm_ctx* ctx, const uint8_t* images, int64_t count, int w, int h,
+                                            int64_t stride, int iters, int b0, double* time, double* memory,
+                                            double* sat);
 /* As qrm_warmup_profile with the transfer stage of host-pipeline mode `mode`
  * (0: zero-copy window fetch, memory[0] = 3 l^2 B/image; 1: full-image copy). */
 QRM_EXPORT qrm_status qrm_warmup_profile_mode(qrm_ctx* ctx, const uint8_t* images, int64_t count, int w, int h,

@@ -33,7 +33,7 @@ ABI_SYMBOLS = (
     "qrm_verify_threshold", "qrm_make_corpus_device", "qrm_patterns_device", "qrm_allocate_streams",
     "qrm_lpt_schedule", "qrm_warmup_profile", "qrm_ctx_set_plan", "qrm_kernel_launch_count",
     "qrm_probe_decode_kernel", "qrm_resample_host", "qrm_extract_float_host", "qrm_hidden_detect_device",
-    "qrm_ctx_set_input_overlap", "qrm_hidden_debug_activation", "qrm_detect_host_timed", "qrm_detect_host_images",
+    "qrm_ctx_set_input_overlap", "qrm_hidden_debug_activation", "qrm_warmup_saturation", "qrm_allocate_streams_sat", "qrm_detect_host_timed", "qrm_detect_host_images",
 )
 
 
@@ -136,6 +136,8 @@ def lib() -> C.CDLL:
         L.qrm_rs_stress_device.argtypes = [i32, i32, i32, u64, i64, vp, vp, vp, vp]
         L.qrm_rs_stress_symbols_device.argtypes = [i32, i32, i32, u64, i64, vp, vp, vp, vp]
         L.qrm_rs_codebook_clear.argtypes = [i32, i32, i32, vp]
+        L.qrm_warmup_saturation.argtypes = [vp, vp, i64, i32, i32, i64, i32, i32, vp, vp, vp]
+        L.qrm_allocate_streams_sat.argtypes = [i32, vp, vp, vp, C.c_double, i32, i32, C.c_double, C.c_double, i32, vp, vp, C.POINTER(C.c_double)]
         L.qrm_rs_encode_packed.argtypes = [i32, i32, i32, u64, C.POINTER(u64)]
         L.qrm_verify_threshold.argtypes = [i32, C.c_double, C.POINTER(i32)]
         L.qrm_make_corpus_device.argtypes = [C.POINTER(_Config), u64, i64, i32, i32, i32, vp, vp]
@@ -690,6 +692,22 @@ class DetectionContext:
                                              m.ctypes.data))
         return t, m
 
+    def warmup_saturation(self, images: np.ndarray | None = None, iters: int = 3, b0: int = 512,
+                          ptr: int | None = None, shape=None):
+        """GPU-aware warm-up (extension): the mode-0 stages on 1, 2 and 4 concurrent
+        streams -> (time[3] ms per b0 on one stream, memory[3] B/image, sat[3] best speedup)."""
+        if images is not None:
+            images = np.ascontiguousarray(images, dtype=np.uint8)
+            B, H, W, _ = images.shape
+            p = images.ctypes.data
+        else:
+            B, H, W = shape
+            p = ptr
+        t, m, sat = np.zeros(3), np.zeros(3), np.zeros(3)
+        _check(lib().qrm_warmup_saturation(self._h, p, B, W, H, H * W * 3, iters, b0, t.ctypes.data,
+                                           m.ctypes.data, sat.ctypes.data))
+        return t, m, sat
+
 
 def detect_host_multi(contexts, images: np.ndarray, first_draw: int = 0, plan=None, mode: int = 0, out=None):
     """qrm_detect_host_multi: one contiguous shard per context (normally one per GPU),
@@ -829,6 +847,22 @@ def allocate_streams(time, memory, b0: float, global_batch: int, stream_budget: 
                                       epsilon, stall_cap, s.ctypes.data, m.ctypes.data, C.byref(bn)))
     return StreamPlan(s.tolist(), m.tolist(), bn.value)
 
+
+def allocate_streams_sat(time, memory, sat, b0: float, global_batch: int, stream_budget: int, m_cap: float,
+                         epsilon: float, stall_cap: int) -> StreamPlan:
+    """Algorithm 1 with the GPU-aware stage model (extension): stage k's speedup from
+    s streams is capped at the measured sat[k]."""
+    K = len(time)
+    t = np.ascontiguousarray(time, np.float64)
+    u = np.ascontiguousarray(memory, np.float64)
+    sa = np.ascontiguousarray(sat, np.float64)
+    s = np.zeros(K, np.int32)
+    m = np.zeros(K, np.int32)
+    bn = C.c_double()
+    _check(lib().qrm_allocate_streams_sat(K, t.ctypes.data, u.ctypes.data, sa.ctypes.data, b0, global_batch,
+                                          stream_budget, m_cap, epsilon, stall_cap, s.ctypes.data, m.ctypes.data,
+                                          C.byref(bn)))
+    return StreamPlan(s.tolist(), m.tolist(), bn.value)
 
 def lpt_schedule(ids, latency, memory, units, stream_count: int, lam: float, m_cap: float, b_min: int,
                  global_batch: int) -> dict:

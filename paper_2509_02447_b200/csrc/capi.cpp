@@ -1876,6 +1876,29 @@ QRM_EXPORT qrm_status qrm_allocate_streams(int stages, const double* time, const
     return QRM_OK;
 }
 
+QRM_EXPORT qrm_status qrm_allocate_streams_sat(int stages, const double* time, const double* memory,
+                                               const double* sat, double b0, int global_batch, int budget,
+                                               double m_cap, double eps, int stall_cap, int* streams_out,
+                                               int* mb_out, double* bottleneck) {
+    if (stages <= 0 || !time || !memory || !sat || !streams_out || !mb_out || !bottleneck)
+        return fail(QRM_INVALID_INPUT, "bad arguments");
+    sched::Profile p;
+    p.b0 = b0;
+    p.time.assign(time, time + stages);
+    p.memory.assign(memory, memory + stages);
+    p.sat.assign(sat, sat + stages);
+    sched::Plan plan;
+    std::string err;
+    const int rc = sched::allocate_streams(p, global_batch, budget, m_cap, eps, stall_cap, plan, err);
+    if (rc) return fail(static_cast<qrm_status>(rc), err);
+    for (int k = 0; k < stages; ++k) {
+        streams_out[k] = plan.streams[k];
+        mb_out[k] = plan.minibatch[k];
+    }
+    *bottleneck = plan.bottleneck;
+    return QRM_OK;
+}
+
 QRM_EXPORT qrm_status qrm_lpt_schedule(int ntasks, const int* ids, const double* lat, const double* mem,
                                        const int* units, int S, double lambda, double m_cap, int b_min, int B,
                                        int capacity, int* p_stream, int* p_id, int* p_units, double* p_lat,
@@ -2010,6 +2033,143 @@ QRM_EXPORT qrm_status qrm_warmup_profile_mode(qrm_ctx* c, const uint8_t* images,
     time[2] = med(t2v);
     c->decode_ms_per_image = time[1] / b0;
     memory[0] = static_cast<double>(mode == 0 ? c->K : img_bytes);
+    memory[1] = static_cast<double>(c->K + sizeof(PendingEntry));
+    memory[2] = static_cast<double>(sizeof(qrm_record));
+    QRM_CUDA(cudaGetLastError());
+    return QRM_OK;
+}
+
+// GPU-aware warm-up (an extension of warmup_profile, not in the reference):
+// each device stage of the mode-0 pipeline (zero-copy window fetch, decode,
+// record D2H) run on s = 1, 2, 4 streams at once, each stream b0 images of its
+// own; sat[k] = the best measured speedup s * T(1) / T(s). A transfer stage
+// bound by the PCIe link shows ~1, a decode of a small mini-batch that leaves
+// SMs idle shows up to s. time[]/memory[] as qrm_warmup_profile_mode (s = 1).
+QRM_EXPORT qrm_status qrm_warmup_saturation(qrm_ctx* c, const uint8_t* images, int64_t count, int w, int h,
+                                            int64_t stride, int iters, int b0, double* time, double* memory,
+                                            double* sat) {
+    qrm_status s = check_uniform(c, images, count, w, h, stride);
+    if (s != QRM_OK) return s;
+    if (iters < 1) return fail(QRM_INVALID_INPUT, "need at least one warm-up iteration");
+    constexpr int kMaxS = 4;
+    if (count < static_cast<int64_t>(kMaxS) * std::max(1, b0))
+        return fail(QRM_INVALID_INPUT, "saturation warm-up needs 4 * b0 images");
+    if ((s = set_device(c->device)) != QRM_OK) return s;
+    b0 = std::max(1, b0);
+    const int64_t img_bytes = static_cast<int64_t>(w) * h * 3;
+    int up, sw, sh, xo, yo;
+    geometry(w, h, up, sw, sh, xo, yo);
+    const int64_t span_bytes = (kMaxS * static_cast<int64_t>(b0) - 1) * stride + img_bytes;
+    const uint8_t* mapped = nullptr;
+    bool reg = false;
+    std::vector<cudaStream_t> sts(kMaxS, nullptr);
+    std::vector<cudaEvent_t> evs;
+    auto cleanup = on_exit([&] {
+        cudaDeviceSynchronize();
+        for (auto e : evs) cudaEventDestroy(e);
+        for (auto st : sts)
+            if (st) cudaStreamDestroy(st);
+        if (reg) cudaHostUnregister(const_cast<uint8_t*>(images));
+    });
+    cudaPointerAttributes attr{};
+    if (cudaPointerGetAttributes(&attr, images) != cudaSuccess || attr.type != cudaMemoryTypeHost) {
+        cudaGetLastError();
+        QRM_CUDA(cudaHostRegister(const_cast<uint8_t*>(images), span_bytes,
+                                  cudaHostRegisterMapped | cudaHostRegisterReadOnly));
+        reg = true;
+    }
+    QRM_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(const_cast<uint8_t**>(&mapped)),
+                                      const_cast<uint8_t*>(images), 0));
+    if (!direct_ok(c, mapped, w, h, stride) || (3 * c->l) % 16 != 0)
+        return fail(QRM_INVALID_INPUT, "window fetch needs 16-B aligned windows");
+    for (auto& st : sts) QRM_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    if (static_cast<int>(c->ws.size()) < 1 + kMaxS) c->ws.resize(1 + kMaxS);
+    for (int j = 0; j < kMaxS; ++j) {
+        Workspace& W = c->ws[1 + j];
+        if ((s = ensure(W.stage, W.stage_cap, static_cast<int64_t>(b0) * c->K)) != QRM_OK) return s;
+        if ((s = workspace_reserve(W, b0)) != QRM_OK) return s;
+    }
+    if ((s = ensure(c->d_records, c->records_cap, kMaxS * static_cast<int64_t>(b0))) != QRM_OK) return s;
+    std::vector<qrm_record> host(static_cast<size_t>(kMaxS) * b0);
+    for (int i = 0; i < 2 * kMaxS + 2; ++i) {
+        cudaEvent_t e;
+        QRM_CUDA(cudaEventCreate(&e));
+        evs.push_back(e);
+    }
+    auto source = [&](int j) {
+        WindowSource hs{};
+        hs.base = mapped + static_cast<int64_t>(j) * b0 * stride;
+        hs.image_stride = stride;
+        hs.pitch = w * 3;
+        hs.x_off = xo;
+        hs.y_off = yo;
+        hs.direct = 1;
+        hs.l = c->l;
+        hs.strategy = c->cfg.tile_strategy;
+        hs.tile_seed = c->cfg.tile_seed;
+        hs.first_draw = static_cast<uint64_t>(j) * b0;
+        return hs;
+    };
+    auto staged = [&](int j) {
+        WindowSource ws = source(j);
+        ws.base = c->ws[1 + j].stage;
+        ws.image_stride = c->K;
+        ws.pitch = 3 * c->l;
+        ws.direct = 0;
+        return ws;
+    };
+    // stage k on `ns` concurrent streams: wall time from the fork to the join (ms)
+    auto run = [&](int k, int ns) -> double {
+        cudaEvent_t fork = evs[0], join = evs[1];
+        QRM_CUDA(cudaEventRecord(fork, sts[0]));
+        for (int j = 1; j < ns; ++j) QRM_CUDA(cudaStreamWaitEvent(sts[j], fork, 0));
+        for (int j = 0; j < ns; ++j) {
+            cudaStream_t st = sts[j];
+            if (k == 0) {
+                if (fetch_stage(c, source(j), w, h, b0, c->ws[1 + j].stage, st) != QRM_OK) return -1.0;
+            } else if (k == 1) {
+                if (run_detect(c, c->ws[1 + j], staged(j), b0, c->d_records + static_cast<int64_t>(j) * b0,
+                               nullptr, nullptr, st, nullptr, nullptr, false) != QRM_OK)
+                    return -1.0;
+            } else {
+                QRM_CUDA(cudaMemcpyAsync(host.data() + static_cast<size_t>(j) * b0,
+                                         c->d_records + static_cast<int64_t>(j) * b0, sizeof(qrm_record) * b0,
+                                         cudaMemcpyDeviceToHost, st));
+            }
+            if (j > 0) {
+                QRM_CUDA(cudaEventRecord(evs[2 + j], st));
+                QRM_CUDA(cudaStreamWaitEvent(sts[0], evs[2 + j], 0));
+            }
+        }
+        QRM_CUDA(cudaEventRecord(join, sts[0]));
+        QRM_CUDA(cudaEventSynchronize(join));
+        float ms = 0.f;
+        QRM_CUDA(cudaEventElapsedTime(&ms, fork, join));
+        return ms;
+    };
+    auto med = [](std::vector<double> v) {
+        std::sort(v.begin(), v.end());
+        return std::max(v[v.size() / 2], 1e-6);
+    };
+    for (int k = 0; k < 3; ++k) {
+        double t1 = 0.0, best = 1.0;
+        for (int ns = 1; ns <= kMaxS; ns *= 2) {
+            run(k, ns);  // untimed: first touch of buffers / lazy state
+            std::vector<double> v;
+            for (int i = 0; i < iters; ++i) {
+                const double ms = run(k, ns);
+                if (ms < 0) return fail(QRM_CUDA_ERROR, "saturation warm-up stage failed");
+                v.push_back(ms);
+            }
+            const double t = med(v);
+            if (ns == 1) t1 = t;
+            else best = std::max(best, ns * t1 / t);
+        }
+        time[k] = t1;
+        sat[k] = best;
+    }
+    c->decode_ms_per_image = time[1] / b0;
+    memory[0] = static_cast<double>(c->K);
     memory[1] = static_cast<double>(c->K + sizeof(PendingEntry));
     memory[2] = static_cast<double>(sizeof(qrm_record));
     QRM_CUDA(cudaGetLastError());

@@ -7,8 +7,11 @@
 namespace qrm::sched {
 
 double stage_time(const Profile& p, int k, int s, int m) {
-    // TIME(k, s, m) = t[k] * (m / b0) / s (sched.cpp:27-30)
-    return p.time[k] * (static_cast<double>(m) / p.b0) / static_cast<double>(s);
+    // TIME(k, s, m) = t[k] * (m / b0) / s (sched.cpp:27-30); with measured
+    // saturation, the s streams' speedup is capped at sat[k].
+    double par = static_cast<double>(s);
+    if (!p.sat.empty()) par = std::min(par, std::max(1.0, p.sat[k]));
+    return p.time[k] * (static_cast<double>(m) / p.b0) / par;
 }
 
 bool mem_ok(const std::vector<int>& s, const std::vector<int>& m, const std::vector<double>& u, double cap) {
@@ -34,6 +37,7 @@ int allocate_streams(const Profile& p, int B, int P, double m_cap, double eps, i
     for (double u : p.memory)
         if (u < 0.0) return err = "per-sample memory must be nonnegative", 1;
     if (P < K) return err = "stream budget below stage count", 1;
+    if (!p.sat.empty() && p.sat.size() != p.time.size()) return err = "profile saturation length mismatch", 1;
     if (B < 1) return err = "global batch must be >= 1", 1;
 
     // (1) one stream per stage; the largest uniform mini-batch that fits M_cap,

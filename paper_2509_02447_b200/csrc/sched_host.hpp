@@ -16,6 +16,10 @@ struct Profile {
     double b0 = 1.0;
     std::vector<double> time;    // t[k] at baseline batch b0
     std::vector<double> memory;  // u[k] per sample
+    // Optional GPU-aware extension (not in the reference): sat[k] = the largest
+    // speedup concurrent streams give stage k (measured: a PCIe-bound transfer
+    // stays near 1). Empty: the reference model, s streams = s times faster.
+    std::vector<double> sat;
 };
 
 struct Plan {
