@@ -853,6 +853,8 @@ def allocate_streams_sat(time, memory, sat, b0: float, global_batch: int, stream
     """Algorithm 1 with the GPU-aware stage model (extension): stage k's speedup from
     s streams is capped at the measured sat[k]."""
     K = len(time)
+    if len(sat) != K or len(memory) != K:
+        raise InvalidInput("profile saturation length mismatch")
     t = np.ascontiguousarray(time, np.float64)
     u = np.ascontiguousarray(memory, np.float64)
     sa = np.ascontiguousarray(sat, np.float64)

@@ -84,6 +84,25 @@ def test_planners_match_reference(kat):
                                c["B"])
 
 
+def test_gpu_aware_allocate_streams(kat):
+    """The saturation-capped Algorithm 1 (extension) equals the reference's when no
+    stage saturates below the stream budget, and never adds streams to a stage
+    whose measured speedup is 1."""
+    for c in kat["allocate_streams"]:
+        if c["rc"] != 0:
+            continue
+        sat = [float(c["P"])] * len(c["time"])
+        p = q.allocate_streams_sat(c["time"], c["memory"], sat, c["b0"], c["B"], c["P"], c["m_cap"], c["eps"],
+                                   c["stall"])
+        assert (p.streams, p.minibatch, p.bottleneck) == (c["streams"], c["minibatch"], c["bottleneck"])
+    t, m = [0.075, 0.022, 0.013], [12288.0, 12304.0, 24.0]
+    ref = q.allocate_streams(t, m, 256.0, 16384, 16, 1e11, 0.0, 2)
+    gpu = q.allocate_streams_sat(t, m, [1.08, 2.02, 1.0], 256.0, 16384, 16, 1e11, 0.0, 2)
+    assert sum(ref.streams) > sum(gpu.streams) and gpu.streams[2] == 1
+    with pytest.raises(q.InvalidInput):
+        q.allocate_streams_sat(t, m, [1.0, 1.0], 256.0, 16384, 16, 1e11, 0.0, 2)
+
+
 def test_allocate_streams_unbounded_cap_documented_divergence():
     """sched.cpp:59 casts floor(M_cap / sum u) to int; for M_cap = 1e18 that is
     undefined (x86: INT_MIN -> InfeasibleConfig, as cmd_bench's own call hits).
