@@ -333,6 +333,9 @@ def main():
     if share:
         local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
+    # multi-GPU: each rank's host threads and pinned pools on its GPU's NUMA node
+    # (at N = 1 rank 0 also times the CPU reference, which wants every core)
+    host_cpus = q.pin_to_device(local) if world > 1 and not share else []
     dist = None
     if world > 1:
         import torch.distributed as dist
@@ -654,6 +657,7 @@ def main():
                           "full_image_h2d (mode 1)": e2e[1]},
             "e2e_plan": {"streams": plan[0], "minibatch": plan[1]},
             "e2e_dropin": e2e_dropin,
+            "host_affinity": {"pinned_to_gpu_numa_node": bool(host_cpus), "cpus": len(host_cpus)},
             "gpu_launches": launches,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                          "frac": achieved / hbm, "traffic": traffic, "kernel": "corr_detect_kernel",

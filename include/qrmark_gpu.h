@@ -124,6 +124,11 @@ typedef struct qrm_ctx qrm_ctx;
 QRM_EXPORT const char* qrm_last_error(void);
 QRM_EXPORT int qrm_abi_version(void);
 QRM_EXPORT int qrm_device_count(void);
+/* Host CPUs on the NUMA node of GPU `device` (sysfs local_cpulist of its PCI
+ * function): *count of them, the first `capacity` written to cpus. *count = 0
+ * when unknown. The multi-GPU host executor pins each shard's host thread (and
+ * each context's staging workers) to these CPUs. */
+QRM_EXPORT qrm_status qrm_device_cpus(int device, int* cpus, int capacity, int* count);
 
 /* ---------------------------------------------------------------- context
  * Replaces DetectionContext::DetectionContext (detect.cpp:135-146) and the

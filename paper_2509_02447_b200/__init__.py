@@ -33,7 +33,7 @@ ABI_SYMBOLS = (
     "qrm_verify_threshold", "qrm_make_corpus_device", "qrm_patterns_device", "qrm_allocate_streams",
     "qrm_lpt_schedule", "qrm_warmup_profile", "qrm_ctx_set_plan", "qrm_kernel_launch_count",
     "qrm_probe_decode_kernel", "qrm_resample_host", "qrm_extract_float_host", "qrm_hidden_detect_device",
-    "qrm_ctx_set_input_overlap", "qrm_hidden_debug_activation", "qrm_warmup_saturation", "qrm_allocate_streams_sat", "qrm_detect_host_timed", "qrm_detect_host_images",
+    "qrm_ctx_set_input_overlap", "qrm_hidden_debug_activation", "qrm_warmup_saturation", "qrm_allocate_streams_sat", "qrm_device_cpus", "qrm_detect_host_timed", "qrm_detect_host_images",
 )
 
 
@@ -138,6 +138,7 @@ def lib() -> C.CDLL:
         L.qrm_rs_codebook_clear.argtypes = [i32, i32, i32, vp]
         L.qrm_warmup_saturation.argtypes = [vp, vp, i64, i32, i32, i64, i32, i32, vp, vp, vp]
         L.qrm_allocate_streams_sat.argtypes = [i32, vp, vp, vp, C.c_double, i32, i32, C.c_double, C.c_double, i32, vp, vp, C.POINTER(C.c_double)]
+        L.qrm_device_cpus.argtypes = [i32, vp, i32, C.POINTER(i32)]
         L.qrm_rs_encode_packed.argtypes = [i32, i32, i32, u64, C.POINTER(u64)]
         L.qrm_verify_threshold.argtypes = [i32, C.c_double, C.POINTER(i32)]
         L.qrm_make_corpus_device.argtypes = [C.POINTER(_Config), u64, i64, i32, i32, i32, vp, vp]
@@ -708,6 +709,23 @@ class DetectionContext:
                                            m.ctypes.data, sat.ctypes.data))
         return t, m, sat
 
+
+def device_cpus(device: int) -> list:
+    """Host CPUs on GPU `device`'s NUMA node ([] when unknown)."""
+    n = C.c_int32()
+    buf = np.zeros(4096, np.int32)
+    _check(lib().qrm_device_cpus(device, buf.ctypes.data, buf.size, C.byref(n)))
+    return buf[:min(n.value, buf.size)].tolist()
+
+
+def pin_to_device(device: int) -> list:
+    """Pin this process to GPU `device`'s NUMA-local CPUs (before allocating pinned
+    host buffers, so first touch lands on that node). Returns the CPU list used."""
+    cpus = device_cpus(device)
+    usable = sorted(set(cpus) & os.sched_getaffinity(0)) if cpus else []
+    if usable:
+        os.sched_setaffinity(0, usable)
+    return usable
 
 def detect_host_multi(contexts, images: np.ndarray, first_draw: int = 0, plan=None, mode: int = 0, out=None):
     """qrm_detect_host_multi: one contiguous shard per context (normally one per GPU),

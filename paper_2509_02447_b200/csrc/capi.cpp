@@ -11,6 +11,8 @@
 // round-robining its mini-batches over plan.streams[k] CUDA streams and
 // cudaEvents instead of queues between stages.
 #include <cuda_runtime.h>
+#include <pthread.h>
+#include <sched.h>
 
 #include <algorithm>
 #include <immintrin.h>
@@ -18,6 +20,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstring>
+#include <fstream>
 #include <map>
 #include <memory>
 #include <mutex>
@@ -69,6 +72,53 @@ cudaError_t launch_corpus(uint64_t first_seed, int64_t count, int w, int h, int 
 }  // namespace qrm
 
 using namespace qrm;
+
+namespace {
+
+// Host CPUs attached to a GPU's NUMA node: /sys/bus/pci/devices/<bus id>/
+// local_cpulist (e.g. "0-55,112-167"). Empty when unknown.
+std::vector<int> device_cpus(int device) {
+    std::vector<int> cpus;
+    char bus[32] = {0};
+    if (cudaDeviceGetPCIBusId(bus, sizeof bus, device) != cudaSuccess) {
+        cudaGetLastError();
+        return cpus;
+    }
+    std::string id(bus);
+    for (auto& ch : id) ch = static_cast<char>(std::tolower(static_cast<unsigned char>(ch)));
+    std::ifstream f("/sys/bus/pci/devices/" + id + "/local_cpulist");
+    std::string list;
+    if (!f || !std::getline(f, list)) return cpus;
+    size_t pos = 0;
+    while (pos < list.size()) {
+        size_t end = list.find(',', pos);
+        if (end == std::string::npos) end = list.size();
+        const std::string part = list.substr(pos, end - pos);
+        const size_t dash = part.find('-');
+        try {
+            const int a = std::stoi(part.substr(0, dash));
+            const int b = dash == std::string::npos ? a : std::stoi(part.substr(dash + 1));
+            for (int c2 = a; c2 <= b && c2 < CPU_SETSIZE; ++c2) cpus.push_back(c2);
+        } catch (...) {
+            return {};
+        }
+        pos = end + 1;
+    }
+    return cpus;
+}
+
+// Pins the calling thread to the GPU's NUMA-local CPUs (no-op when unknown):
+// its page-locked buffers are then first-touched on, and read from, that node.
+void pin_thread_to_device(int device) {
+    const std::vector<int> cpus = device_cpus(device);
+    if (cpus.empty()) return;
+    cpu_set_t set;
+    CPU_ZERO(&set);
+    for (int c2 : cpus) CPU_SET(c2, &set);
+    pthread_setaffinity_np(pthread_self(), sizeof set, &set);
+}
+
+}  // namespace
 
 namespace {
 
@@ -788,7 +838,9 @@ qrm_status detect_host_impl(qrm_ctx* c, const uint8_t* images, int64_t count, in
         if (mode == 3 && !c->copy_stream) QRM_CUDA(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
         if (!c->pool) {
             const unsigned hc = std::thread::hardware_concurrency();
-            c->pool = std::make_unique<HostPool>(static_cast<int>(std::max(1u, std::min(hc ? hc - 1 : 1u, 31u))));
+            const int dev = c->device;
+            c->pool = std::make_unique<HostPool>(static_cast<int>(std::max(1u, std::min(hc ? hc - 1 : 1u, 31u))),
+                                                 [dev] { pin_thread_to_device(dev); });
         }
         for (int j = 0; j < s1; ++j) {
             Workspace& W = c->ws[1 + j];
@@ -1156,14 +1208,14 @@ QRM_EXPORT qrm_status qrm_detect_host_multi(qrm_ctx* const* ctxs, int nctx, cons
     std::vector<std::string> err(nctx);
     std::vector<qrm_host_stats> part(nctx);
     auto run = [&](int i) {
+        pin_thread_to_device(ctxs[i]->device);  // each shard's host thread on its GPU's NUMA node
         const int64_t b = count * i / nctx, e = count * (i + 1) / nctx;
         st[i] = qrm_detect_host(ctxs[i], images + b * stride, e - b, w, h, stride, first_draw + static_cast<uint64_t>(b),
                                 out + b, plan, mode, &part[i]);
         if (st[i] != QRM_OK) err[i] = g_err;  // thread-local: carried to the caller below
     };
-    std::vector<std::thread> th;
-    for (int i = 1; i < nctx; ++i) th.emplace_back(run, i);
-    run(0);
+    std::vector<std::thread> th;  // one thread per shard (the caller's own affinity stays untouched)
+    for (int i = 0; i < nctx; ++i) th.emplace_back(run, i);
     for (auto& t : th) t.join();
     for (int i = 0; i < nctx; ++i)
         if (st[i] != QRM_OK) return fail(st[i], "shard " + std::to_string(i) + ": " + err[i]);
@@ -1873,6 +1925,14 @@ QRM_EXPORT qrm_status qrm_allocate_streams(int stages, const double* time, const
         mb_out[k] = plan.minibatch[k];
     }
     *bottleneck = plan.bottleneck;
+    return QRM_OK;
+}
+
+QRM_EXPORT qrm_status qrm_device_cpus(int device, int* cpus, int capacity, int* count) {
+    if (!count || (capacity > 0 && !cpus)) return fail(QRM_INVALID_INPUT, "bad arguments");
+    const std::vector<int> v = device_cpus(device);
+    *count = static_cast<int>(v.size());
+    for (int i = 0; i < capacity && i < static_cast<int>(v.size()); ++i) cpus[i] = v[i];
     return QRM_OK;
 }
 

@@ -14,8 +14,12 @@ namespace qrm {
 
 class HostPool {
 public:
-    explicit HostPool(int threads) {
-        for (int i = 0; i < threads; ++i) workers_.emplace_back([this] { loop(); });
+    explicit HostPool(int threads, std::function<void()> init = {}) {
+        for (int i = 0; i < threads; ++i)
+            workers_.emplace_back([this, init] {
+                if (init) init();  // e.g. pin the worker to the GPU's NUMA node
+                loop();
+            });
     }
     ~HostPool() {
         {
