@@ -251,7 +251,7 @@ struct qrm_ctx {
     std::vector<cudaEvent_t> timing_events;  // the same with timing, for calls that report stage spans
     double hybrid_fraction = 0.5;        // mode 3: share of each mini-batch fetched zero-copy
     int64_t stage_piece = 512;           // modes 2/3: windows gathered per H2D
-    int64_t stage_grain = 32;            // modes 2/3: windows per host-worker task
+    int64_t stage_grain = 8;             // modes 2/3: windows per host-worker task (sweep: 8 best)
     double decode_ms_per_image = 0.0;  // from the last warm-up profile (Algorithm 2 latencies)
     int extractor = QRM_EXTRACTOR_SPREAD_SPECTRUM;  // qrm_ctx_set_extractor
     bool input_overlap = false;  // qrm_ctx_set_input_overlap
@@ -943,13 +943,28 @@ qrm_status detect_host_impl(qrm_ctx* c, const uint8_t* images, int64_t count, in
             for (int64_t p0 = 0; p0 < cnt - nz; p0 += piece) {
                 const int64_t p1 = std::min(cnt - nz, p0 + piece);
                 c->pool->parallel_for(p1 - p0, c->stage_grain, [&](int64_t j0, int64_t j1) {
-                    for (int64_t i = p0 + j0; i < p0 + j1; ++i) {
+                    auto window_at = [&](int64_t i) {
                         const int64_t img = first + nz + i;
                         int tx, ty;
                         select_tile(kWorkingSize, kWorkingSize, l, cfg.tile_strategy, cfg.tile_seed,
                                     first_draw + static_cast<uint64_t>(img), tx, ty);
-                        const uint8_t* src0 = image_at(img) + static_cast<int64_t>(yo + ty) * pitch +
-                                              static_cast<int64_t>(xo + tx) * 3;
+                        return image_at(img) + static_cast<int64_t>(yo + ty) * pitch + static_cast<int64_t>(xo + tx) * 3;
+                    };
+                    // The windows' rows are cold (each image is read once): prefetch the
+                    // next window's 64 rows while this one is copied, so the worker has a
+                    // whole window of line fills in flight instead of one row's.
+                    const uint8_t* next = j0 < j1 ? window_at(p0 + j0) : nullptr;
+                    for (int64_t i = p0 + j0; i < p0 + j1; ++i) {
+                        const uint8_t* src0 = next;
+                        next = i + 1 < p0 + j1 ? window_at(i + 1) : nullptr;
+                        if (next && rowb == 192)
+                            for (int r = 0; r < 64; ++r) {
+                                const char* row = reinterpret_cast<const char*>(next + static_cast<int64_t>(r) * pitch);
+                                _mm_prefetch(row, _MM_HINT_T0);
+                                _mm_prefetch(row + 64, _MM_HINT_T0);
+                                _mm_prefetch(row + 128, _MM_HINT_T0);
+                                _mm_prefetch(row + 191, _MM_HINT_T0);
+                            }
                         uint8_t* dst = hst + i * K;
                         if (rowb == 192) {
                             // l = 64: non-temporal 16-B stores. Staging written through
