@@ -412,6 +412,42 @@ def main():
     # time (back-to-back launches overlap through programmatic dependent launch).
     # An isolated launch (events around each launch, no overlap) is reported too.
     kern_ms = ctx.kernel_time_probe(pool[:BATCH], reps=max(10, args.steps // 2))
+
+    # The same device-resident step on a mixed corpus: per 4096-image batch 1/4
+    # clean watermarked, 1/4 blurred watermarked (bit errors -> RS corrections),
+    # 1/2 unwatermarked (RS failures, exact-zero correlation ties), so the timed
+    # region runs every record path, not only the zero-syndrome early exit.
+    mixed = None
+    try:
+        mq = BATCH // 4
+        mix_batches = []
+        for b in range(4):
+            pos = q.make_corpus(cfg, 900000 + rank * 100000 + b * BATCH, 2 * mq)
+            neg = q.make_corpus(cfg, 2000000 + rank * 100000 + b * BATCH, BATCH - 2 * mq, embed=False)
+            mix_batches.append(torch.cat([pos[:mq], q.apply_attack(pos[mq:], "blur", 1.0), neg]).contiguous())
+        for i in range(args.warmup):
+            ctx.detect_device(mix_batches[i % 4], first_draw=i * BATCH, out=out)
+        torch.cuda.synchronize()
+        mrec = q.records_from_device(out)
+        barrier()
+        m0, m1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        m0.record(stream)
+        for i in range(args.steps):
+            ctx.detect_device(mix_batches[i % 4], first_draw=(i * world + rank) * BATCH, out=out)
+        m1.record(stream)
+        torch.cuda.synchronize()
+        mms = max_over_ranks(m0.elapsed_time(m1))
+        mixed = {"value": world * BATCH * args.steps / (mms / 1e3), "unit": "images/s",
+                 "ms_per_step": mms / args.steps,
+                 "corpus": "per batch: 1/4 clean watermarked, 1/4 blurred watermarked, 1/2 unwatermarked",
+                 "records_last_warmup_batch": {
+                     "decoded": int((mrec["status"] == 1).sum()),
+                     "corrected": int(((mrec["status"] == 1) & (mrec["errors"] > 0)).sum()),
+                     "failed": int((mrec["status"] == 0).sum()), "with_ties": int((mrec["ties"] > 0).sum()),
+                     "verified": int(mrec["verified"].sum())}}
+        del mix_batches
+    except Exception as exc:
+        mixed = {"unavailable": str(exc)}
     hbm, peak_kind = _peaks()
     alg_bytes = BATCH * (ctx.window_bytes + q.RECORD_DTYPE.itemsize)
     launch_ms = ms / launches if launches else ms_step  # this rank: one decode launch per step
@@ -659,6 +695,7 @@ def main():
             "e2e_dropin": e2e_dropin,
             "host_affinity": {"pinned_to_gpu_numa_node": bool(host_cpus), "cpus": len(host_cpus)},
             "gpu_launches": launches,
+            "value_mixed_corpus": mixed,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                          "frac": achieved / hbm, "traffic": traffic, "kernel": "corr_detect_kernel",
                          "kernel_ms": launch_ms, "peak_kind": peak_kind,

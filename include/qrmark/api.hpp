@@ -34,6 +34,13 @@
 namespace qrmark {
 
 // ------------------------------------------------------------- errors.hpp
+// Departures from the reference's accepted inputs (both raise InvalidInput):
+//  * detection (DetectionContext, detect_one, detect_batch) with codewords
+//    wider than 64 bits, e.g. gf256-dynamic with payload_bits >= 56: records
+//    and the fused decode epilogue hold the raw word in one u64;
+//  * bw_decode on codes with t > 31 (e.g. CodeParams::make(gf256, 255, 190)):
+//    the batched GPU decoder keeps the error locator in one warp's lanes.
+// Every default and every SPEC.md code is inside both limits.
 class InvalidInput : public std::invalid_argument {
 public:
     explicit InvalidInput(const std::string& w) : std::invalid_argument(w) {}
