@@ -284,10 +284,10 @@ def config512_submetric(q, ctx, cfg, world, rank, max_over_ranks, warmup, batch=
     recs = recs_pin.numpy().view(q.RECORD_DTYPE).reshape(-1)
     calls = batch // pool_n
 
-    def run(pl, steps):
+    def run(pl, steps, lpt=None):
         for i in range(steps * calls):
             ctx.detect_host(None, (i * world + rank) * pool_n, plan=pl, mode=0, out=recs, ptr=host.data_ptr(),
-                            shape=(pool_n, 512, 512))
+                            shape=(pool_n, 512, 512), lpt=lpt)
             assert recs["verified"].all()
 
     out = {"workload": "configs[2]: 512x512 RGB, batch 16384 (8 calls x 2048 over a pinned pool), one 64x64 tile "
@@ -295,16 +295,23 @@ def config512_submetric(q, ctx, cfg, world, rank, max_over_ranks, warmup, batch=
            "warmup_profile_ms_per_16": [float(x) for x in t], "warmup_bytes_per_image": [float(x) for x in m],
            "saturation_warmup": {"b0": 256, "ms_per_b0_one_stream": [float(x) for x in ts],
                                  "best_speedup_on_1_2_4_streams": [float(x) for x in sat]}}
-    for name, pl in (("alg1", (plan.streams, [max(1, min(pool_n, x)) for x in plan.minibatch])),
-                     ("alg1_gpu_aware", (plan_gpu.streams, [max(1, min(pool_n, x)) for x in plan_gpu.minibatch])),
-                     ("baseline_111", ([1, 1, 1], [pool_n] * 3))):
-        run(pl, max(1, warmup // 3))
+    # Algorithm 2 (lpt_schedule, sched.cpp:177-235) driving the executor: 512-image
+    # mini-batches as tasks (latency from the warm-up profile) placed and sharded
+    # over the decode streams (lambda 0.2, b_min 128)
+    for name, pl, lpt in (("alg1", (plan.streams, [max(1, min(pool_n, x)) for x in plan.minibatch]), None),
+                          ("alg1_gpu_aware", (plan_gpu.streams, [max(1, min(pool_n, x)) for x in plan_gpu.minibatch]),
+                           None),
+                          ("alg2_lpt", ([2, 2, 1], [512] * 3), (0.2, 128)),
+                          ("baseline_111", ([1, 1, 1], [pool_n] * 3), None)):
+        run(pl, max(1, warmup // 3), lpt)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        run(pl, 2)
+        run(pl, 2, lpt)
         dt = max_over_ranks(time.perf_counter() - t0)
         out[name] = {"plan": {"streams": list(pl[0]), "minibatch": list(pl[1])},
                      "e2e_images_per_s": world * 2 * batch / dt}
+        if lpt is not None:
+            out[name]["lpt"] = {"lambda": lpt[0], "b_min": lpt[1]}
     return out
 
 
