@@ -11,7 +11,7 @@
 // sum_px float(v/127.5-1) P is the sign of the EXACT integer
 //   S = sum_px (2v - 255) P = 2 D - 255 colsum(P)
 // except when S == 0, where the reference's double rounding decides; those
-// (image, bit) pairs are re-evaluated exactly (tie_bit_exact below; for codes
+// (image, bit) pairs are re-evaluated exactly (tie_bit_exact, qrm_window.cuh; for codes
 // the epilogue cannot finish, by detect_finish_kernel), so hard bits are
 // bit-exact.
 //
@@ -77,7 +77,8 @@ struct TieEntry {
 };
 struct TieList {
     TieEntry ties[kCorrM];
-    long long lut[256];  // float(v/127.5 - 1) * 2^31, exact integers
+    int32_t elut[kTieLutWords];  // tie residual table, one copy per smem bank (qrm_window.cuh)
+    int32_t red[kCorrThreads / 32];  // per-warp partial dot products
 };
 constexpr int kRedBytes = kCorrM * kRedStride * 4;
 static_assert(kRedBytes + sizeof(TieList) <= kCorrStages * kCorrStageBytes, "end-of-kernel buffers exceed the ring");
@@ -139,47 +140,34 @@ __device__ __forceinline__ void finish_image(const DetectParams& p, CorrSmem& sm
     store_record(p.out + img, rec);
 }
 
-// Exact reference hard bit of a zero integer correlation. The reference sums
-// double(float(v/127.5 - 1)) * P sequentially (stego.cpp:60-64) and tests
-// soft > 0 (stego.cpp:12). Every term is a multiple of 2^-31 (the float ulp at
-// |d| >= 1/255) and |sum| < 2^16, so every partial sum is exact in double and
-// the reference's result is the exact sum: an int64 dot product of the window
-// with P through the table lut[v] = d(v) * 2^31, in any order (lane-parallel).
-__device__ __forceinline__ bool tie_bit_exact(const WindowSource& s, int64_t img, int K, const int8_t* pat,
-                                              const long long* lut, int lane) {
-    const uint8_t* wb = window_base(s, img, K);
-    const int row_bytes = 3 * s.l;
-    const int pitch = s.direct ? s.pitch : row_bytes;
-    long long acc = 0;
-    for (int px = lane; px < K; px += 32) {
-        const int trow = px / row_bytes;
-        const long long d = lut[wb[static_cast<int64_t>(trow) * pitch + (px - trow * row_bytes)]];
-        acc += pat[px] > 0 ? d : -d;
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    return acc > 0;
-}
-
-// t = 1 codes: the CTA's images with tied bits (collected by finish_image),
-// one warp per image — resolve the tied bits, then RS + verify + record.
+// t = 1 codes: the CTA's images with tied bits (collected by finish_image).
+// Each tied bit is one exact dot product over the window, computed by the
+// whole CTA (every thread's chunk loads in flight at once), then thread 0
+// runs RS + verify + the record.
 __device__ __noinline__ void finish_ties(const DetectParams& p, CorrSmem& sm, TieList& tl, int warp, int lane) {
-    for (int v = threadIdx.x; v < 256; v += kCorrThreads) {
-        const float d = __double2float_rn(__dsub_rn(__ddiv_rn(static_cast<double>(v), 127.5), 1.0));
-        tl.lut[v] = __double2ll_rn(static_cast<double>(d) * 2147483648.0);
-    }
+    tie_lut_fill(tl.elut, threadIdx.x, kCorrThreads);
     __syncthreads();
     griddep_wait();  // the previous grid is done with the records
     const int nb = p.nbits;
-    for (int e = warp; e < sm.nties; e += kCorrThreads / 32) {
+    const int nties = sm.nties;
+    for (int e = 0; e < nties; ++e) {  // CTA-uniform
         const TieEntry te = tl.ties[e];
         uint64_t raw = te.raw;
-        for (uint64_t m = te.tie_mask; m; m &= m - 1) {
+        for (uint64_t m = te.tie_mask; m; m &= m - 1) {  // CTA-uniform
             const int b = __ffsll(static_cast<long long>(m)) - 1;
-            if (tie_bit_exact(p.src, te.image, p.K, p.patterns + static_cast<int64_t>(b) * p.K_pad, tl.lut, lane))
-                raw |= 1ull << (nb - 1 - b);
+            int32_t part = tie_dot_partial(p.src, te.image, p.K, p.patterns + static_cast<int64_t>(b) * p.K_pad,
+                                           tl.elut, threadIdx.x, kCorrThreads);
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+            if (lane == 0) tl.red[warp] = part;
+            __syncthreads();
+            int32_t tot = 0;
+#pragma unroll
+            for (int w = 0; w < kCorrThreads / 32; ++w) tot += tl.red[w];
+            __syncthreads();  // tl.red is reused by the next bit
+            if (tot > 0) raw |= 1ull << (nb - 1 - b);
         }
-        if (lane == 0) {
+        if (threadIdx.x == 0) {
             if (p.raw_out) p.raw_out[te.image] = raw;
             uint64_t cw = 0;
             const int nerr = rs_t1_packed(sm.rs, raw, cw);

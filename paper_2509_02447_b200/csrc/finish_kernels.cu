@@ -1,5 +1,5 @@
 // Completion and staging kernels of the detection path (sm_100a):
-//  * detect_finish_kernel — exact tie resolution + general-t RS + verify for
+//  * detect_finish_kernel — exact tie resolution (tie_bit_exact, qrm_window.cuh) + general-t RS + verify for
 //    the records the decode kernel (corr_kernel.cu) left pending;
 //  * gather_windows_kernel / resample_kernel — the preprocess geometry
 //    (bilinear upscale, centre crop, transforms.cpp:24-84) evaluated only on
@@ -13,36 +13,23 @@
 
 namespace qrm {
 
-// Exact reference hard bit for a zero integer correlation: the reference sums
-// double(float(v/127.5 - 1)) * P sequentially over px (stego.cpp:60-64) and
-// tests soft > 0 (stego.cpp:12); replay that exact summation order.
-__device__ __forceinline__ bool reference_tie_bit(const WindowSource& s, int64_t img, int K, const int8_t* pat) {
-    const uint8_t* wb = window_base(s, img, K);
-    const int row_bytes = 3 * s.l;
-    const int pitch = s.direct ? s.pitch : row_bytes;
-    double acc = 0.0;
-    for (int px = 0; px < K; ++px) {
-        const int trow = px / row_bytes;
-        const uint8_t v = wb[static_cast<int64_t>(trow) * pitch + (px - trow * row_bytes)];
-        const double d = static_cast<double>(__double2float_rn(__dsub_rn(__ddiv_rn(static_cast<double>(v), 127.5), 1.0)));
-        acc = pat[px] > 0 ? __dadd_rn(acc, d) : __dsub_rn(acc, d);
-    }
-    return acc * (1.0 / static_cast<double>(K)) > 0.0;
-}
-
 // Completes pending records: resolves exact-zero correlations bit-exactly,
 // then RS-corrects (t = 1 closed form or warp Berlekamp-Massey) and verifies.
 // One warp per pending image; lane b re-evaluates tied bit b.
 template <int TMAX>
 __global__ void __launch_bounds__(256) detect_finish_kernel(const __grid_constant__ DetectParams p) {
     __shared__ RsSmem T;
+    __shared__ int32_t elut[kTieLutWords];  // tie_bit_exact's residual table (qrm_window.cuh)
     __shared__ int npend_s;
     griddep_wait();               // the decode grid's records and pending list are complete
     griddep_launch_dependents();  // the next decode may start its prologue
     if (threadIdx.x == 0) npend_s = *reinterpret_cast<volatile int32_t*>(p.pending_count);
     __syncthreads();
     const int npend = npend_s;
-    if (npend > 0) rs_stage_tables(T, p.rs, threadIdx.x, blockDim.x);  // nothing to do: skip the staging
+    if (npend > 0) {  // nothing to do: skip the staging
+        rs_stage_tables(T, p.rs, threadIdx.x, blockDim.x);
+        tie_lut_fill(elut, threadIdx.x, blockDim.x);
+    }
     __syncthreads();
     const int lane = threadIdx.x & 31;
     const int64_t warps = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
@@ -51,17 +38,11 @@ __global__ void __launch_bounds__(256) detect_finish_kernel(const __grid_constan
         const PendingEntry pe = p.pending[e];
         uint64_t raw = p.out[pe.image].raw;
         const int nb = p.nbits;
-        for (int b0 = 0; b0 < nb; b0 += 32) {
-            const int b = b0 + lane;
-            uint64_t setbit = 0;
-            if (b < nb && ((pe.tie_mask >> b) & 1)) {
-                const bool bit = reference_tie_bit(p.src, pe.image, p.K, p.patterns + static_cast<int64_t>(b) * p.K_pad);
-                setbit = static_cast<uint64_t>(bit) << (nb - 1 - b);
-            }
-            // OR-reduce the resolved bits (tied bits were 0 in raw)
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) setbit |= __shfl_xor_sync(0xffffffffu, setbit, o);
-            raw |= setbit;
+        // each tied bit by the whole warp (exact int64 dot product; tied bits are 0 in raw)
+        for (uint64_t m = pe.tie_mask; m; m &= m - 1) {
+            const int b = __ffsll(static_cast<long long>(m)) - 1;
+            if (tie_bit_exact(p.src, pe.image, p.K, p.patterns + static_cast<int64_t>(b) * p.K_pad, elut, lane))
+                raw |= 1ull << (nb - 1 - b);
         }
         if (p.raw_out && lane == 0) p.raw_out[pe.image] = raw;
         int nerr;
