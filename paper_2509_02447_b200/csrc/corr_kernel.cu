@@ -28,6 +28,7 @@
 
 #include <atomic>
 #include <cstdlib>
+#include <type_traits>
 
 #include "qrm_device.cuh"
 #include "qrm_launch.h"
@@ -85,36 +86,48 @@ static_assert(kRedBytes + sizeof(TieList) <= kCorrStages * kCorrStageBytes, "end
 
 constexpr size_t kCorrSmemBytes = 1024 /*align slack*/ + kCorrStages * kCorrStageBytes + sizeof(CorrSmem);
 
-// Epilogue for one image (one TMEM lane): S_i = 2 D_i - 255 colsum_i; bit i =
-// S_i > 0 (harden), tie i = S_i == 0; pack MSB-first; t = 1 code without ties:
-// RS-correct + verify in registers. Straight-line: bits are gathered with
-// constant shifts and reversed once (the packed word is MSB-first).
-__device__ __forceinline__ void finish_image(const DetectParams& p, CorrSmem& sm, TieList& tl, int64_t img,
-                                             const uint32_t (&acc)[kCorrN]) {
+// Epilogue, part 1: columns [c0, c0 + NC) of one image. S_i = 2 D_i - 255
+// colsum_i; bit i = S_i > 0 (harden), tie i = S_i == 0, as 64-bit column masks
+// (bit i = column i); soft values for those columns when asked.
+template <int NC>
+__device__ __forceinline__ void image_columns(const DetectParams& p, const CorrSmem& sm, int64_t img, int c0,
+                                              const uint32_t (&acc)[NC], uint64_t& pos, uint64_t& zer) {
     const int nb = p.nbits;
-    uint32_t pos[2] = {0u, 0u}, zer[2] = {0u, 0u};
-    const int4* thr4 = reinterpret_cast<const int4*>(sm.thr);
+    pos = 0;
+    zer = 0;
+    const int4* thr4 = reinterpret_cast<const int4*>(sm.thr + c0);
 #pragma unroll
-    for (int q = 0; q < kCorrN / 4; ++q) {
+    for (int q = 0; q < NC / 4; ++q) {
         const int4 t = thr4[q];
         const int tv[4] = {t.x, t.y, t.z, t.w};
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
             const int i = 4 * q + u;
             const int s2 = 2 * static_cast<int>(acc[i]) - tv[u];
-            pos[i >> 5] |= static_cast<uint32_t>(s2 > 0) << (i & 31);
-            zer[i >> 5] |= static_cast<uint32_t>(s2 == 0) << (i & 31);
+            pos |= static_cast<uint64_t>(s2 > 0) << i;
+            zer |= static_cast<uint64_t>(s2 == 0) << i;
         }
     }
-    const uint64_t nmask = nb >= 64 ? ~0ull : ((1ull << nb) - 1);
-    const uint64_t tmask = ((static_cast<uint64_t>(zer[1]) << 32) | zer[0]) & nmask;
-    const uint64_t raw = __brevll((static_cast<uint64_t>(pos[1]) << 32) | pos[0]) >> (64 - nb);
+    pos <<= c0;
+    zer <<= c0;
     if (p.soft) {
         const double inv = 1.0 / (255.0 * static_cast<double>(p.K));
 #pragma unroll
-        for (int i = 0; i < kCorrN; ++i)  // constant indices keep acc[] in registers
-            if (i < nb) p.soft[img * nb + i] = static_cast<double>(2 * static_cast<int>(acc[i]) - sm.thr[i]) * inv;
+        for (int i = 0; i < NC; ++i)  // constant indices keep acc[] in registers
+            if (c0 + i < nb)
+                p.soft[img * nb + c0 + i] = static_cast<double>(2 * static_cast<int>(acc[i]) - sm.thr[c0 + i]) * inv;
     }
+}
+
+// Epilogue, part 2: pack MSB-first; t = 1 code without ties: RS-correct +
+// verify in registers and write the record. Tied images go to the CTA's tie
+// list (finish_ties); codes the epilogue cannot finish, to the pending list.
+__device__ __forceinline__ void finish_masks(const DetectParams& p, CorrSmem& sm, TieList& tl, int64_t img,
+                                             uint64_t pos, uint64_t zer) {
+    const int nb = p.nbits;
+    const uint64_t nmask = nb >= 64 ? ~0ull : ((1ull << nb) - 1);
+    const uint64_t tmask = zer & nmask;
+    const uint64_t raw = __brevll(pos) >> (64 - nb);
     if (p.raw_out) p.raw_out[img] = raw;
     qrm_record rec;
     if (tmask == 0 && p.fuse_t1) {
@@ -290,7 +303,11 @@ __global__ void __launch_bounds__(kCorrThreads, 1) corr_detect_kernel(const __gr
         if (S == 1) {
             griddep_wait();  // the previous completion kernel is done with records / the pending list
             const int64_t img = m0 + row;
-            if (row < tile_m && img < p.count) finish_image(p, sm, tl, img, acc);
+            if (row < tile_m && img < p.count) {
+                uint64_t pos, zer;
+                image_columns<kCorrN>(p, sm, img, 0, acc, pos, zer);
+                finish_masks(p, sm, tl, img, pos, zer);
+            }
         } else {
             // push this partial row to its owner CTA: slot `rank`, local row
             const uint32_t owner = static_cast<uint32_t>(row / rows_per);
@@ -334,25 +351,44 @@ __global__ void __launch_bounds__(kCorrThreads, 1) corr_detect_kernel(const __gr
     }
     if (S > 1) {
         cluster_sync_all();  // every partial row has landed in its owner's smem
-        if (tid < rows_per) {
+        // All producer threads reduce: S images' worth of threads per image row
+        // would idle, so each of the 128/rows_per threads of an image sums a
+        // column slice over the S partials and the slices' masks are OR-ed
+        // across the group (consecutive lanes) before one lane finishes it.
+        if (tid < kCorrProducers) {
             griddep_wait();  // the previous completion kernel is done with records / the pending list
-            uint32_t acc[kCorrN];
-#pragma unroll
-            for (int i = 0; i < kCorrN; ++i) acc[i] = 0;
-            for (uint32_t s = 0; s < S; ++s) {
-                const int4* src = reinterpret_cast<const int4*>(&red[(s * rows_per + tid) * kRedStride]);
-#pragma unroll
-                for (int q = 0; q < kCorrN / 4; ++q) {
-                    const int4 v = src[q];
-                    acc[4 * q] += v.x;
-                    acc[4 * q + 1] += v.y;
-                    acc[4 * q + 2] += v.z;
-                    acc[4 * q + 3] += v.w;
-                }
-            }
-            const int row = static_cast<int>(rank) * rows_per + tid;
+            const int per = kCorrProducers / rows_per;  // S threads per image (rows_per = 128 / S)
+            const int r = tid / per, part = tid % per;
+            const int row = static_cast<int>(rank) * rows_per + r;
             const int64_t img = m0 + row;
-            if (row < tile_m && img < p.count) finish_image(p, sm, tl, img, acc);
+            uint64_t pos = 0, zer = 0;
+            auto slice = [&](auto nc_tag) {
+                constexpr int NC = decltype(nc_tag)::value;
+                const int c0 = part * NC;
+                uint32_t acc[NC];
+#pragma unroll
+                for (int i = 0; i < NC; ++i) acc[i] = 0;
+                for (uint32_t s = 0; s < S; ++s) {
+                    const int4* src = reinterpret_cast<const int4*>(&red[(s * rows_per + r) * kRedStride + c0]);
+#pragma unroll
+                    for (int q = 0; q < NC / 4; ++q) {
+                        const int4 v = src[q];
+                        acc[4 * q] += v.x;
+                        acc[4 * q + 1] += v.y;
+                        acc[4 * q + 2] += v.z;
+                        acc[4 * q + 3] += v.w;
+                    }
+                }
+                if (row < tile_m && img < p.count) image_columns<NC>(p, sm, img, c0, acc, pos, zer);
+            };
+            if (per == 8) slice(std::integral_constant<int, kCorrN / 8>{});       // S = 8 (forced)
+            else if (per == 4) slice(std::integral_constant<int, kCorrN / 4>{});  // S = 4
+            else slice(std::integral_constant<int, kCorrN / 2>{});                // S = 2
+            for (int o = 1; o < per; o <<= 1) {  // the group's lanes are consecutive
+                pos |= __shfl_xor_sync(0xffffffffu, pos, o);
+                zer |= __shfl_xor_sync(0xffffffffu, zer, o);
+            }
+            if (part == 0 && row < tile_m && img < p.count) finish_masks(p, sm, tl, img, pos, zer);
         }
     }
     __syncthreads();
