@@ -403,6 +403,10 @@ def main():
                 torch.cuda.synchronize()
         torch.cuda.synchronize()
         launches0 = q.kernel_launch_count()
+        # a short device spin ahead of the start event, so the host has queued
+        # the first steps when the timed region opens (the region then holds
+        # the K steps' device time, not the host's first-launch latency)
+        torch.cuda._sleep(200_000)
         e0.record(stream)
         for i in range(args.steps):
             step(args.warmup + i)
@@ -438,6 +442,7 @@ def main():
         mrec = q.records_from_device(out)
         barrier()
         m0, m1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda._sleep(200_000)
         m0.record(stream)
         for i in range(args.steps):
             ctx.detect_device(mix_batches[i % 4], first_draw=(i * world + rank) * BATCH, out=out)
