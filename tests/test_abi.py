@@ -129,3 +129,20 @@ def test_null_context_calls_report_invalid_input():
     assert L.qrm_ctx_set_extractor(None, 0, 7) == invalid
     assert L.qrm_detect_device(None, None, 0, 256, 256, 196608, 0, None, None) == invalid
     assert "null context" in L.qrm_last_error().decode()
+
+
+def test_multitile_tasks_and_predictors():
+    """build_tasks / WarmupStats (sched.cpp:126-155): latency and memory scale with tile area."""
+    import numpy as np
+    from paper_2509_02447_b200.multitile import (ConstantTilePredictor, ContrastTilePredictor, WarmupStats,
+                                                 build_tasks)
+    st = WarmupStats(64, 2.0, 12288.0)
+    assert st.latency_for(32) == 0.5 and st.latency_for(128) == 8.0 and st.memory_for(80) == 12288.0 * 1.5625
+    imgs = [np.zeros((512, 512, 3), np.uint8), np.full((512, 512, 3), 7, np.uint8)]
+    assert build_tasks(imgs, ConstantTilePredictor(80), st) == [(0, 80, 3.125, 19200.0), (1, 80, 3.125, 19200.0)]
+    flat = ContrastTilePredictor()
+    assert flat.select_tile_size(imgs[0]) == 128  # no contrast: the largest tile
+    noisy = np.random.default_rng(0).integers(0, 256, (512, 512, 3), dtype=np.uint8)
+    assert flat.select_tile_size(noisy) == 32
+    with pytest.raises(q.InvalidInput):
+        build_tasks(imgs, ConstantTilePredictor(0), st)
