@@ -78,7 +78,7 @@ struct TieEntry {
 };
 struct TieList {
     TieEntry ties[kCorrM];
-    int32_t elut[kTieLutWords];  // tie residual table, one copy per smem bank (qrm_window.cuh)
+    int32_t elut[kTieLutWords];  // tie residual table (qrm_window.cuh)
     int32_t red[kCorrThreads / 32];  // per-warp partial dot products
 };
 constexpr int kRedBytes = kCorrM * kRedStride * 4;

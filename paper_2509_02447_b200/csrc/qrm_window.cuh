@@ -30,11 +30,12 @@ __device__ __forceinline__ const uint8_t* window_base(const WindowSource& s, int
 // and E(v) is 255 * 2^31 times float's rounding error of (2v - 255)/255:
 // |E| <= 255 * 64, so the dot product fits int32 and has the reference's sign.
 //
-// The E table is replicated once per bank (elut[v * 32 + lane]) so the
-// per-byte lookups of a warp never conflict. tie_dot_partial: thread t of nt
-// takes 16-byte chunks t, t + nt, ... of the window and of the pattern row,
-// loading 8 chunks before using any.
-constexpr int kTieLutWords = 256 * 32;
+// tie_dot_partial: thread t of nt takes 16-byte chunks t, t + nt, ... of the
+// window and of the pattern row, loading 8 chunks before using any. The E
+// table is 256 int32 in shared memory: a bank-replicated copy (32 KB) made the
+// lookups conflict-free but cost more to fill (1.9 us per CTA) than the
+// conflicts of a 1 KB table cost in lookups.
+constexpr int kTieLutWords = 256;
 
 // float(v/127.5 - 1) equals (2v - 255) / 255.f (IEEE single division) for all
 // 256 v, and the single division is far cheaper than the double one.
@@ -44,13 +45,8 @@ __device__ __forceinline__ int32_t tie_residual(int v) {
     return static_cast<int32_t>(255ll * L - static_cast<long long>(2 * v - 255) * 2147483648ll);
 }
 
-// Fills the replicated table: 256 residuals, then the copies (barriers inside:
-// every thread of the block calls it).
 __device__ __forceinline__ void tie_lut_fill(int32_t* elut, int tid, int nthreads) {
-    for (int v = tid; v < 256; v += nthreads) elut[v << 5] = tie_residual(v);
-    __syncthreads();
-    for (int i = tid; i < kTieLutWords; i += nthreads)
-        if (i & 31) elut[i] = elut[i & ~31];
+    for (int v = tid; v < kTieLutWords; v += nthreads) elut[v] = tie_residual(v);
 }
 
 __device__ __forceinline__ int32_t tie_dot_partial(const WindowSource& s, int64_t img, int K, const int8_t* pat,
@@ -58,7 +54,6 @@ __device__ __forceinline__ int32_t tie_dot_partial(const WindowSource& s, int64_
     const uint8_t* wb = window_base(s, img, K);
     const int row_bytes = 3 * s.l;
     const int pitch = s.direct ? s.pitch : row_bytes;
-    const int32_t* mylut = elut + (t & 31);
     int32_t acc = 0;
     const bool vec = ((reinterpret_cast<uintptr_t>(wb) | reinterpret_cast<uintptr_t>(pat) |
                        static_cast<uintptr_t>(pitch) | static_cast<uintptr_t>(row_bytes)) & 15) == 0;
@@ -83,7 +78,7 @@ __device__ __forceinline__ int32_t tie_dot_partial(const WindowSource& s, int64_
                 for (int w = 0; w < 4; ++w)
 #pragma unroll
                     for (int k = 0; k < 4; ++k) {
-                        const int32_t e = mylut[((vw[w] >> (8 * k)) & 0xFF) << 5];
+                        const int32_t e = elut[(vw[w] >> (8 * k)) & 0xFF];
                         const int32_t pv = static_cast<int8_t>((qw[w] >> (8 * k)) & 0xFF);  // +1, -1 (0: padding)
                         acc += e * pv;
                     }
@@ -92,7 +87,7 @@ __device__ __forceinline__ int32_t tie_dot_partial(const WindowSource& s, int64_
     } else {
         for (int px = t; px < K; px += nt) {
             const int trow = px / row_bytes;
-            const int32_t e = mylut[static_cast<int>(wb[static_cast<int64_t>(trow) * pitch + (px - trow * row_bytes)]) << 5];
+            const int32_t e = elut[wb[static_cast<int64_t>(trow) * pitch + (px - trow * row_bytes)]];
             acc += e * static_cast<int32_t>(pat[px]);
         }
     }
