@@ -61,6 +61,7 @@ cudaError_t launch_rs_stress_symbols(const RsTables* tab, const uint8_t* gpar, i
                                      cudaStream_t st);
 cudaError_t launch_rs_stress(const RsTables* tab, const uint64_t* enc_mask, uint64_t seed, int64_t count,
                              uint64_t* msg, uint64_t* words, int8_t* nerr_true, cudaStream_t st);
+cudaError_t launch_swizzle_patterns(const int8_t* pat, int K_pad, int8_t* out, cudaStream_t st);
 cudaError_t launch_build_patterns(uint64_t seed, int nbits, int K, int K_pad, int8_t* pat, int32_t* colsum,
                                   cudaStream_t st);
 cudaError_t launch_residual(uint64_t seed, int nbits, int K, uint64_t codeword, float* delta, cudaStream_t st);
@@ -238,6 +239,7 @@ struct qrm_ctx {
     uint64_t key_cw = 0, key_msg = 0;
     int tau_msg = 0, tau_raw = 0;
     int8_t* d_patterns = nullptr;
+    int8_t* d_patterns_sw = nullptr;  // per-chunk SW128 smem images of the pattern operand (one bulk copy per stage)
     int32_t* d_colsum = nullptr;
     const RsTables* d_rs = nullptr;
     qrm_record* d_records = nullptr;
@@ -319,6 +321,7 @@ DetectParams base_params(qrm_ctx* c, Workspace& w, int64_t count, qrm_record* ou
     p.key_cw = c->key_cw;
     p.key_msg = c->key_msg;
     p.patterns = c->d_patterns;
+    p.patterns_sw = c->d_patterns_sw;
     p.colsum = c->d_colsum;
     p.rs = c->d_rs;
     p.out = out;
@@ -533,6 +536,8 @@ QRM_EXPORT qrm_status qrm_ctx_create(int device, const qrm_config* cfg, qrm_ctx*
     QRM_CUDA(cudaMalloc(&c->d_patterns, static_cast<size_t>(kMaxNBits) * c->K_pad));
     QRM_CUDA(cudaMalloc(&c->d_colsum, sizeof(int32_t) * kMaxNBits));
     QRM_LAUNCH(launch_build_patterns(cfg->key_seed, nbits, c->K, c->K_pad, c->d_patterns, c->d_colsum, nullptr));
+    QRM_CUDA(cudaMalloc(&c->d_patterns_sw, static_cast<size_t>(kMaxNBits) * c->K_pad));
+    QRM_LAUNCH(launch_swizzle_patterns(c->d_patterns, c->K_pad, c->d_patterns_sw, nullptr));
     QRM_CUDA(cudaDeviceSynchronize());
     c->ws.resize(1);
     *out = c.release();
@@ -549,6 +554,7 @@ QRM_EXPORT void qrm_ctx_destroy(qrm_ctx* c) {
     for (auto e : c->timing_events) cudaEventDestroy(e);
     if (c->host_records) cudaFreeHost(c->host_records);
     cudaFree(c->d_patterns);
+    cudaFree(c->d_patterns_sw);
     cudaFree(c->d_colsum);
     cudaFree(c->d_records);
     cudaFree(c->hid.w_sw);

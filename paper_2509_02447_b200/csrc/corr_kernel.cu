@@ -217,7 +217,7 @@ __global__ void __launch_bounds__(kCorrThreads, 1) corr_detect_kernel(const __gr
     if (warp == 4) tmem_alloc<kCorrN>(&sm.tmem_base);
     if (tid == 0) {
         for (int s = 0; s < kCorrStages; ++s) {
-            mbar_init(&sm.full[s], kCorrProducers);
+            mbar_init(&sm.full[s], kCorrProducers + 1);  // + thread 0's expect_tx arrival for the pattern bulk copy
             mbar_init(&sm.empty[s], 1);
         }
         mbar_init(&sm.accum_full, 1);
@@ -260,6 +260,11 @@ __global__ void __launch_bounds__(kCorrThreads, 1) corr_detect_kernel(const __gr
             mbar_wait(&sm.empty[s], ((it / kCorrStages) & 1) ^ 1);
             const uint32_t a_s = ring_u32 + s * kCorrStageBytes;
             const uint32_t b_s = a_s + kCorrABytes;
+            if (tid == 0) {  // the stage's pattern operand: one bulk copy of its pre-swizzled smem image
+                mbar_arrive_expect_tx(&sm.full[s], kCorrBBytes);
+                bulk_load(b_s, p.patterns_sw + static_cast<int64_t>(kc_begin + it) * kCorrBBytes, kCorrBBytes,
+                          &sm.full[s]);
+            }
             if (kbyte < p.K) {
                 const int64_t off = static_cast<int64_t>(trow) * pitch + tcol;
                 // .L2::64B: fill only the 64-B sector pairs the 192-B row covers (the
@@ -267,11 +272,6 @@ __global__ void __launch_bounds__(kCorrThreads, 1) corr_detect_kernel(const __gr
 #pragma unroll
                 for (int j = 0; j < 8; ++j)
                     if (valid[j]) cp_async16_l2_64(a_s + sw128_offset(rb + 16 * j, c), wb[j] + off);
-            }
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                const int n = rb + 16 * j;
-                cp_async16(b_s + sw128_offset(n, c), p.patterns + static_cast<int64_t>(n) * p.K_pad + kbyte);
             }
             // Never block on the copies: the barrier phase completes when every
             // producer's copies for this stage have landed.
@@ -471,6 +471,27 @@ cudaError_t launch_corr_detect(const DetectParams& p_in, int sm_count, cudaStrea
     cudaLaunchAttribute attr[2];
     cudaLaunchConfig_t cfg = corr_config(static_cast<unsigned>(tiles) * S, S, st, attr);
     return cudaLaunchKernelEx(&cfg, corr_detect_kernel, p);
+}
+
+// The pattern operand per 128-byte K chunk as the exact shared-memory image the
+// MMA reads (64 rows x 128 B, 128B-swizzled K-major): chunk kc at
+// out + kc * 8 KB, so a stage fetches it with one bulk copy instead of 512
+// 16-byte cp.async.
+__global__ void swizzle_patterns_kernel(const int8_t* __restrict__ pat, int K_pad, int8_t* __restrict__ out) {
+    const int64_t total = static_cast<int64_t>(K_pad / kCorrKC) * kCorrN * (kCorrKC / 16);
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int c = static_cast<int>(i % (kCorrKC / 16));
+        const int n = static_cast<int>((i / (kCorrKC / 16)) % kCorrN);
+        const int64_t kc = i / (kCorrKC / 16) / kCorrN;
+        const uint4 v = *reinterpret_cast<const uint4*>(pat + static_cast<int64_t>(n) * K_pad + kc * kCorrKC + c * 16);
+        *reinterpret_cast<uint4*>(out + kc * kCorrBBytes + sw128_offset(n, c)) = v;
+    }
+}
+
+cudaError_t launch_swizzle_patterns(const int8_t* pat, int K_pad, int8_t* out, cudaStream_t st) {
+    swizzle_patterns_kernel<<<148, 256, 0, st>>>(pat, K_pad, out);
+    return cudaGetLastError();
 }
 
 size_t corr_smem_bytes() { return kCorrSmemBytes; }

@@ -83,6 +83,7 @@ struct DetectParams {
     int32_t ksplit;       // launcher: forced split-K cluster size (0: automatic)
     uint64_t key_cw, key_msg;
     const int8_t* patterns;   // [64][K_pad] s8, rows >= nbits zero
+    const int8_t* patterns_sw;  // the same, per 128-byte K chunk: [K_pad/128][64 x 128 B SW128 smem image]
     const int32_t* colsum;    // [64] sum_px P_i[px]
     const RsTables* rs;
     qrm_record* out;
