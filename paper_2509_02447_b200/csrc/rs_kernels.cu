@@ -205,7 +205,7 @@ __global__ void __launch_bounds__(256) rs_seg_packed_kernel(const RsTables* __re
 // General t, symbol bytes: one codeword per segment of W lanes (n <= 32), or
 // per warp with P symbols per lane (n <= 32 P).
 template <int TMAX, int W, int P>
-__global__ void __launch_bounds__(256) rs_seg_symbols_kernel(const RsTables* __restrict__ g,
+__global__ void __launch_bounds__(256, (W == 32 && TMAX >= 16) ? 2 : 1) rs_seg_symbols_kernel(const RsTables* __restrict__ g,
                                                             const uint8_t* __restrict__ recv, int64_t count,
                                                             uint8_t* __restrict__ cw_out,
                                                             int8_t* __restrict__ nerr_out) {
