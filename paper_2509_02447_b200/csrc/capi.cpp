@@ -613,6 +613,11 @@ QRM_EXPORT qrm_status qrm_probe_decode_kernel(qrm_ctx* c, const uint8_t* images,
     QRM_CUDA(cudaEventCreate(&g_probe[1]));
     double total = 0.0;
     for (int i = 0; i < reps && s == QRM_OK; ++i) {
+        // a 50 us device spin first, so the decode is already queued when its
+        // start event runs: the probe times the launch on the device, not the
+        // host's submission latency (~10 us, which an event-to-event span
+        // around a lone launch otherwise includes)
+        QRM_LAUNCH(launch_stage_load(50000, nullptr));
         s = detect_uniform(c, c->ws[0], images, count, w, h, stride, static_cast<uint64_t>(i) * count, c->d_records,
                            nullptr, nullptr, nullptr, nullptr, nullptr, true);  // resident images, decodes only
         cudaEventSynchronize(g_probe[1]);

@@ -167,6 +167,25 @@ def test_t2_code_detect(qrm, cuda, ref):
     assert rec["verified"][:48].all()
 
 
+def test_ties_through_general_t_completion_kernel(qrm, cuda, ref):
+    """A t = 2 code leaves records to detect_finish_kernel, which resolves tied bits
+    with the warp-wide exact dot product: every tied image equals the reference."""
+    key = oracle.Oracle().default_message(1, 44)
+    cfg = qrm.DetectionConfig(code=qrm.CodeParams.make(4, 15, 11), key_message=key)
+    oc = oracle.DetectCfg(key_message=key, mnk=(4, 15, 11))
+    imgs = qrm.make_corpus(cfg, 91000, 2048, embed=False)
+    with qrm.DetectionContext(cfg) as ctx:
+        rec = qrm.records_from_device(ctx.detect_device(imgs))
+    tied = np.nonzero(rec["ties"])[0]
+    assert tied.size > 0, "corpus produced no ties; enlarge it"
+    host = imgs.cpu().numpy()
+    for i in tied:
+        Ri = ref.detect_sequential([host[i]], oc, first_draw=int(i))
+        assert oracle.bits_to_word(Ri["raw_bits"][0]) == int(rec["raw"][i])
+        assert bool(Ri["verified"][0]) == bool(rec["verified"][i])
+        assert int(Ri["errors"][0]) == int(rec["errors"][i])
+
+
 def test_512_centre_crop_and_ragged_upscale(qrm, cuda, ref, cfg):
     """512^2 (direct centre-crop window) and mixed/small sizes (bilinear upscale path)."""
     big = qrm.make_corpus(cfg, 9000, 16, w=512, h=512)
