@@ -412,7 +412,8 @@ QRM_EXPORT qrm_status qrm_warmup_profile(qrm_ctx* ctx, const uint8_t* images, in
 /* GPU-aware warm-up (extension): the mode-0 stages (window fetch, decode,
  * record D2H) each on 1, 2 and 4 concurrent streams of b0 images (host images,
  * count >= 4 b0). time[3] = ms per b0 images on one stream, memory[3] bytes
- * per image, sat[3] = best speedup s T(1) / T(s) (1 = no gain from streams). */
+ * per image, sat[3] = best speedup s T(1) / T(s) (1 = no gain from streams;
+ * speedups under 10 % count as none, being within run-to-run noise). */
 QRM_EXPORT qrm_status qrm_warmup_saturation(qrm_ctx* ctx, const uint8_t* images, int64_t count, int w, int h,
                                             int64_t stride, int iters, int b0, double* time, double* memory,
                                             double* sat);

@@ -2252,7 +2252,8 @@ QRM_EXPORT qrm_status qrm_warmup_saturation(qrm_ctx* c, const uint8_t* images, i
             else best = std::max(best, ns * t1 / t);
         }
         time[k] = t1;
-        sat[k] = best;
+        // speedups under 10 % are run-to-run noise, not concurrency: report none
+        sat[k] = best < 1.10 ? 1.0 : best;
     }
     c->decode_ms_per_image = time[1] / b0;
     memory[0] = static_cast<double>(c->K);
