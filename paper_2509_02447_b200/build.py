@@ -75,7 +75,7 @@ def build(verbose: bool = False, ptxas_verbose: bool = False) -> str:
         for f in [ex.submit(_run, cmd, verbose or ptxas_verbose) for cmd in jobs]:
             f.result()
     if _stale(LIB, objs):
-        _run([NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-Xcompiler", "-fPIC", "-lpthread"], verbose)
+        _run([NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-Xcompiler", "-fPIC", "-lpthread", "-ldl"], verbose)
     return LIB
 
 

@@ -34,6 +34,7 @@
 #include "qrm_types.h"
 #include "qrmark_gpu.h"
 #include <cudaTypedefs.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include "host_pool.hpp"
 #include "qrm_hidden.h"
@@ -73,6 +74,20 @@ cudaError_t launch_corpus(uint64_t first_seed, int64_t count, int w, int h, int 
 }  // namespace qrm
 
 using namespace qrm;
+
+namespace {
+
+// NVTX ranges (tracing): host-side spans of the executor's
+// calls, mini-batches and staging, visible in Nsight Systems / ncu; free when
+// no tool is attached (NVTX v3 is header-only and dispatches lazily).
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
+};
+
+}  // namespace
 
 namespace {
 
@@ -588,6 +603,7 @@ QRM_EXPORT qrm_status qrm_ctx_set_plan(qrm_ctx* c, const qrm_plan* plan) {
 
 QRM_EXPORT qrm_status qrm_detect_device(qrm_ctx* c, const uint8_t* images, int64_t count, int w, int h,
                                         int64_t stride, uint64_t first_draw, qrm_record* out, void* stream) {
+    NvtxRange range("qrm_detect_device");
     qrm_status s = check_uniform(c, images, count, w, h, stride);
     if (s != QRM_OK) return s;
     if (count > 0 && !out) return fail(QRM_INVALID_INPUT, "null record buffer");
@@ -750,6 +766,7 @@ qrm_status detect_host_impl(qrm_ctx* c, const uint8_t* images, int64_t count, in
                             uint64_t first_draw, qrm_record* out, const qrm_plan* plan, int mode,
                             qrm_host_stats* stats, const std::vector<HostPiece>* pieces,
                             const HostCallOpts& opt = HostCallOpts{}) {
+    NvtxRange call_range("qrm_detect_host");
     qrm_status s;
     if (opt.ptrs) {
         if (!c) return fail(QRM_INVALID_INPUT, "null context");
@@ -886,6 +903,7 @@ qrm_status detect_host_impl(qrm_ctx* c, const uint8_t* images, int64_t count, in
     double h2d = 0.0;
     int launches0 = static_cast<int>(g_launches.load());
     for (int64_t b = 0; b < nwork; ++b) {
+        NvtxRange mb_range("mini-batch");
         const int64_t first = pieces ? (*pieces)[b].first : b * mb;
         const int64_t cnt = pieces ? (*pieces)[b].count : std::min(mb, count - first);
         const int lane = pieces ? (*pieces)[b].stream : static_cast<int>(b % s1);
@@ -953,6 +971,7 @@ qrm_status detect_host_impl(qrm_ctx* c, const uint8_t* images, int64_t count, in
             const int64_t piece = c->stage_piece;
             for (int64_t p0 = 0; p0 < cnt - nz; p0 += piece) {
                 const int64_t p1 = std::min(cnt - nz, p0 + piece);
+                NvtxRange gather_range("stage windows (host gather)");
                 c->pool->parallel_for(p1 - p0, c->stage_grain, [&](int64_t j0, int64_t j1) {
                     auto window_at = [&](int64_t i) {
                         const int64_t img = first + nz + i;
