@@ -12,7 +12,7 @@ The reference defines the pieces but never runs them on real work:
   memory come from the warm-up statistics scaled by (tile / 64)^2;
 - ``lpt_schedule`` (the C++ planner, bit-exact with the reference's) places and
   shards the tasks over S streams;
-- one host thread per stream runs its pieces in placement order through the
+- one host thread per stream (a pool kept across calls) runs its pieces in placement order through the
   native executor (``qrm_detect_host_images``: only each image's window
   crosses PCIe). Each stream owns one context per tile size, because a
   context is single-size like the reference's (detect.hpp:114).
@@ -30,8 +30,8 @@ row 3 describes.
 from __future__ import annotations
 
 import dataclasses
-import threading
 import time
+from concurrent.futures import ThreadPoolExecutor
 from dataclasses import dataclass
 
 import numpy as np
@@ -130,8 +130,10 @@ class MultiTileDetector:
         self.ctx = [{l: DetectionContext(dataclasses.replace(cfg, tile_size=l), device=device)
                      for l in self.tile_sizes} for _ in range(self.streams)]
         self.stats = WarmupStats()
+        self.pool = ThreadPoolExecutor(self.streams)  # one host thread per stream, kept across calls
 
     def close(self):
+        self.pool.shutdown(wait=True)
         for per in self.ctx:
             for c in per.values():
                 c.close()
@@ -199,11 +201,8 @@ class MultiTileDetector:
             except Exception as exc:  # surfaced to the caller below
                 errors.append(exc)
 
-        th = [threading.Thread(target=run, args=(s,)) for s in range(self.streams)]
-        for t in th:
-            t.start()
-        for t in th:
-            t.join()
+        for f in [self.pool.submit(run, s) for s in range(self.streams)]:
+            f.result()
         if errors:
             raise errors[0]
         return out, {"sizes": sizes, "pieces": per_stream, "loads": sch["loads"],
@@ -246,11 +245,8 @@ class MultiTileDetector:
             except Exception as exc:
                 errors.append(exc)
 
-        th = [threading.Thread(target=run, args=(s,)) for s in range(self.streams)]
-        for t in th:
-            t.start()
-        for t in th:
-            t.join()
+        for f in [self.pool.submit(run, s) for s in range(self.streams)]:
+            f.result()
         if errors:
             raise errors[0]
         return out, {"pieces": per_stream, "loads": sch["loads"], "counts": counts}
