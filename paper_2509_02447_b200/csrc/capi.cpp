@@ -883,6 +883,54 @@ qrm_status detect_host_impl(qrm_ctx* c, const uint8_t* images, int64_t count, in
         }
     }
 
+    // One mini-batch, zero-copy transfer: the whole call on one stream. The
+    // decode launches behind the window fetch (programmatic dependent launch,
+    // its producers wait for the fetch) and writes the records straight into
+    // the page-locked host buffer, so there are no cross-stream event hops and
+    // no D2H copy: ~50 -> ~35 us of fixed cost per call.
+    if (!pieces && nmb == 1 && mode == 0 && !opt.ptrs && !opt.times && load_ns[0] == 0 && load_ns[1] == 0 &&
+        load_ns[2] == 0 && !up && dimg && c->extractor == QRM_EXTRACTOR_SPREAD_SPECTRUM &&
+        direct_ok(c, dimg, w, h, stride) && (3 * c->l) % 16 == 0) {
+        qrm_record* dout = nullptr;
+        if (cudaHostGetDevicePointer(reinterpret_cast<void**>(&dout), hout, 0) == cudaSuccess && dout) {
+            cudaStream_t st = c->streams[0];
+            nstreams_used = 1;
+            Workspace& W = c->ws[1];
+            if ((s = ensure(W.stage, W.stage_cap, count * c->K)) != QRM_OK) return s;
+            const int launches0 = static_cast<int>(g_launches.load());
+            WindowSource hs{};
+            hs.base = dimg;
+            hs.image_stride = stride;
+            hs.pitch = w * 3;
+            hs.x_off = xo;
+            hs.y_off = yo;
+            hs.direct = 1;
+            hs.l = c->l;
+            hs.strategy = c->cfg.tile_strategy;
+            hs.tile_seed = c->cfg.tile_seed;
+            hs.first_draw = first_draw;
+            if ((s = fetch_stage(c, hs, w, h, count, W.stage, st)) != QRM_OK) return s;
+            WindowSource ws = hs;
+            ws.base = W.stage;
+            ws.image_stride = c->K;
+            ws.pitch = 3 * c->l;
+            ws.direct = 0;
+            if ((s = run_detect(c, W, ws, count, dout, nullptr, nullptr, st, nullptr, nullptr, true)) != QRM_OK)
+                return s;
+            QRM_CUDA(cudaStreamSynchronize(st));
+            if (hout != out) std::memcpy(out, hout, sizeof(qrm_record) * count);
+            if (stats) {
+                stats->wall_ms = static_cast<double>(now_ns() - t0) / 1e6;
+                stats->h2d_bytes = static_cast<double>(c->K) * count;
+                stats->d2h_bytes = static_cast<double>(sizeof(qrm_record)) * count;
+                stats->minibatches = 1;
+                stats->kernel_launches = static_cast<int>(g_launches.load()) - launches0;
+            }
+            return QRM_OK;
+        }
+        cudaGetLastError();
+    }
+
     nstreams_used = nstreams;
     const int64_t nwork = pieces ? static_cast<int64_t>(pieces->size()) : nmb;
     // events come from the context's pools (creating ~20 per call cost ~50 us);
