@@ -296,12 +296,14 @@ def config512_submetric(q, ctx, cfg, world, rank, max_over_ranks, warmup, batch=
            "saturation_warmup": {"b0": 256, "ms_per_b0_one_stream": [float(x) for x in ts],
                                  "best_speedup_on_1_2_4_streams": [float(x) for x in sat]}}
     # Algorithm 2 (lpt_schedule, sched.cpp:177-235) driving the executor: 512-image
-    # mini-batches as tasks (latency from the warm-up profile) placed and sharded
-    # over the decode streams (lambda 0.2, b_min 128)
+    # mini-batches as tasks (latency from the warm-up profile) placed over the
+    # decode streams. lambda = inf (plain LPT): a finite slack shards the tasks
+    # into b_min pieces whose per-call cost showed (scripts/lpt_settings.py:
+    # lambda 0.2 -> 2.33 M, inf -> 2.86 M img/s against 3.03 M single-stream)
     for name, pl, lpt in (("alg1", (plan.streams, [max(1, min(pool_n, x)) for x in plan.minibatch]), None),
                           ("alg1_gpu_aware", (plan_gpu.streams, [max(1, min(pool_n, x)) for x in plan_gpu.minibatch]),
                            None),
-                          ("alg2_lpt", ([2, 2, 1], [512] * 3), (0.2, 128)),
+                          ("alg2_lpt", ([2, 2, 1], [512] * 3), (float("inf"), 128)),
                           ("baseline_111", ([1, 1, 1], [pool_n] * 3), None)):
         run(pl, max(1, warmup // 3), lpt)
         torch.cuda.synchronize()
@@ -311,7 +313,7 @@ def config512_submetric(q, ctx, cfg, world, rank, max_over_ranks, warmup, batch=
         out[name] = {"plan": {"streams": list(pl[0]), "minibatch": list(pl[1])},
                      "e2e_images_per_s": world * 2 * batch / dt}
         if lpt is not None:
-            out[name]["lpt"] = {"lambda": lpt[0], "b_min": lpt[1]}
+            out[name]["lpt"] = {"lambda": "inf" if lpt[0] == float("inf") else lpt[0], "b_min": lpt[1]}
     # Multi-tile interleaving: per-image tile sizes {32, 64, 128} (a third of the
     # images each, each embedded with its size), Algorithm 2 placing 1024-image
     # tasks of each size on 3 streams (one context per size per stream). The
