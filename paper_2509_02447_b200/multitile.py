@@ -112,6 +112,33 @@ def build_tasks(images, predictor: TileSizePredictor, stats: WarmupStats):
     return tasks
 
 
+def schedule_groups(counts, stats: WarmupStats, streams: int, minibatch: int, lam: float, b_min: int):
+    """Algorithm 2 over per-size groups: each group of counts[l] images is cut into
+    mini-batch tasks (latency / memory from the warm-up statistics), lpt_schedule
+    places and shards them over `streams` streams, and each piece becomes a
+    contiguous range (size, first, count) of its group. Returns (per-stream
+    piece lists in placement order, stream loads)."""
+    tasks = []
+    for l in sorted(counts):
+        for a in range(0, counts[l], minibatch):
+            tasks.append((l, a, min(minibatch, counts[l] - a)))
+    per_stream = [[] for _ in range(streams)]
+    if not tasks:
+        return per_stream, [0.0] * streams
+    lat = [stats.latency_for(l) * c for (l, _, c) in tasks]
+    mem = [stats.memory_for(l) * c for (l, _, c) in tasks]
+    sch = lpt_schedule(list(range(len(tasks))), lat, mem, [c for (_, _, c) in tasks], streams, lam,
+                       float(1 << 40), b_min, sum(counts.values()))
+    offset = [0] * len(tasks)
+    for (st, tid, units, _, _, _) in sch["pieces"]:
+        l, a, _ = tasks[tid]
+        per_stream[st].append((l, a + offset[tid], units))
+        offset[tid] += units
+    if offset != [c for (_, _, c) in tasks]:
+        raise RuntimeError("schedule does not cover the batch")
+    return per_stream, sch["loads"]
+
+
 class MultiTileDetector:
     """Per-image tile sizes, Algorithm 2 placement over `streams` CUDA streams.
 
@@ -171,25 +198,8 @@ class MultiTileDetector:
             if s not in self.tile_sizes:
                 raise InvalidInput(f"predicted tile size {s} has no context")
         groups = {l: [i for i in range(n) if sizes[i] == l] for l in self.tile_sizes}
-        # mini-batch tasks per size group: (size, first index in the group, count)
-        tasks = []
-        for l in self.tile_sizes:
-            g = groups[l]
-            for a in range(0, len(g), minibatch):
-                tasks.append((l, a, min(minibatch, len(g) - a)))
-        lat = [self.stats.latency_for(l) * c for (l, _, c) in tasks]
-        mem = [self.stats.memory_for(l) * c for (l, _, c) in tasks]
-        sch = lpt_schedule(list(range(len(tasks))), lat, mem, [c for (_, _, c) in tasks], self.streams, lam,
-                           float(1 << 40), b_min, n)
-        # pieces of a task are consecutive ranges of its group in placement order
-        offset = [0] * len(tasks)
-        per_stream = [[] for _ in range(self.streams)]
-        for (st, tid, units, _, _, _) in sch["pieces"]:
-            l, a, _ = tasks[tid]
-            per_stream[st].append((l, a + offset[tid], units))
-            offset[tid] += units
-        if offset != [c for (_, _, c) in tasks]:
-            raise RuntimeError("schedule does not cover the batch")
+        per_stream, loads = schedule_groups({l: len(groups[l]) for l in self.tile_sizes}, self.stats, self.streams,
+                                            minibatch, lam, b_min)
         errors = []
 
         def run(s):
@@ -205,7 +215,7 @@ class MultiTileDetector:
             f.result()
         if errors:
             raise errors[0]
-        return out, {"sizes": sizes, "pieces": per_stream, "loads": sch["loads"],
+        return out, {"sizes": sizes, "pieces": per_stream, "loads": loads,
                      "counts": {l: len(groups[l]) for l in self.tile_sizes}}
 
     def detect_grouped(self, groups, shape, lam: float = 0.2, b_min: int = 128, minibatch: int = 512):
@@ -218,22 +228,9 @@ class MultiTileDetector:
         img_bytes = H * W * 3
         counts = {l: int(groups[l][1]) if l in groups else 0 for l in self.tile_sizes}
         out = {l: np.zeros(counts[l], dtype=RECORD_DTYPE) for l in self.tile_sizes}
-        tasks = []
-        for l in self.tile_sizes:
-            for a in range(0, counts[l], minibatch):
-                tasks.append((l, a, min(minibatch, counts[l] - a)))
-        if not tasks:
+        if not any(counts.values()):
             return out, {"pieces": [], "counts": counts}
-        lat = [self.stats.latency_for(l) * c for (l, _, c) in tasks]
-        mem = [self.stats.memory_for(l) * c for (l, _, c) in tasks]
-        sch = lpt_schedule(list(range(len(tasks))), lat, mem, [c for (_, _, c) in tasks], self.streams, lam,
-                           float(1 << 40), b_min, sum(counts.values()))
-        offset = [0] * len(tasks)
-        per_stream = [[] for _ in range(self.streams)]
-        for (st, tid, units, _, _, _) in sch["pieces"]:
-            l, a, _ = tasks[tid]
-            per_stream[st].append((l, a + offset[tid], units))
-            offset[tid] += units
+        per_stream, loads = schedule_groups(counts, self.stats, self.streams, minibatch, lam, b_min)
         errors = []
 
         def run(s):
@@ -249,4 +246,4 @@ class MultiTileDetector:
             f.result()
         if errors:
             raise errors[0]
-        return out, {"pieces": per_stream, "loads": sch["loads"], "counts": counts}
+        return out, {"pieces": per_stream, "loads": loads, "counts": counts}

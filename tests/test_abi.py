@@ -146,3 +146,21 @@ def test_multitile_tasks_and_predictors():
     assert flat.select_tile_size(noisy) == 32
     with pytest.raises(q.InvalidInput):
         build_tasks(imgs, ConstantTilePredictor(0), st)
+
+
+@pytest.mark.parametrize("counts,streams,mb,lam,bmin", [({32: 683, 64: 683, 128: 682}, 3, 512, 0.2, 128),
+                                                        ({32: 10, 64: 0, 128: 1000}, 2, 256, float("inf"), 64),
+                                                        ({64: 4096}, 4, 1024, 0.0, 512)])
+def test_multitile_schedule_covers_every_image(counts, streams, mb, lam, bmin):
+    """Algorithm 2 over per-size groups (multitile.schedule_groups): the pieces are
+    contiguous ranges that cover every image of every group exactly once."""
+    from paper_2509_02447_b200.multitile import WarmupStats, schedule_groups
+    per_stream, loads = schedule_groups(counts, WarmupStats(64, 0.01, 12288.0), streams, mb, lam, bmin)
+    assert len(per_stream) == streams and len(loads) == streams
+    for l, c in counts.items():
+        covered = sorted((a, a + k) for st in per_stream for (ll, a, k) in st if ll == l)
+        pos = 0
+        for a, b in covered:
+            assert a == pos and b > a
+            pos = b
+        assert pos == c
