@@ -208,7 +208,7 @@ __device__ __forceinline__ void seg_syndromes(const RsSmem& T, const uint32_t (&
     const int sl = lane & (W - 1);
 #pragma unroll
     for (int j = 0; j < RMAX; ++j) S[j] = 0;
-#pragma unroll
+#pragma unroll(P > 4 ? 1 : P)  // long codes: a rolled position loop keeps the code in the I-cache
     for (int p = 0; p < P; ++p) {
         const int i = sl + W * p;
         const uint32_t v = sym[p];
@@ -442,7 +442,7 @@ __device__ __forceinline__ int warp_locate_lp(const RsSmem& T, const uint32_t (&
     }
     int roots = 0, changed = 0;
     bool badlane = false;
-#pragma unroll
+#pragma unroll 1  // rolled: the unrolled 8-position Chien/Forney body overflowed the I-cache (ncu: 92 % no_instructions)
     for (int p = 0; p < P; ++p) {
         const int i = lane + 32 * p;
         err[p] = 0;
